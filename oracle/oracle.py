@@ -1,0 +1,268 @@
+"""CPU oracle -- TEST INFRASTRUCTURE ONLY.
+
+Restates the reference gZCCL codec (``/root/reference/pkg/src/gzccl/codec.py``)
+in plain C (``gz_oracle.c``, loaded here through ctypes) and the reference
+collective schedules (``collectives.py``) in numpy over that codec.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+leg may import this module; the product package never does.  It is pinned
+against golden vectors produced by the reference itself
+(``tests/golden/make_golden.py``) in ``tests/test_oracle.py``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import struct
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libgz_oracle.so")
+
+BLOCK = 32
+HEADER_BYTES = 24
+_SC_HDR = struct.Struct("<QQQ")  # collectives.py:29
+
+
+class OracleDecodeError(ValueError):
+    pass
+
+
+def build() -> str:
+    """Compile the C oracle in place (make)."""
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB_PATH
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        u64, i64, p = ctypes.c_uint64, ctypes.c_int64, ctypes.c_void_p
+        L.gzo_compress_bound.restype = u64
+        L.gzo_compress_bound.argtypes = [u64]
+        L.gzo_compress.restype = ctypes.c_int
+        L.gzo_compress.argtypes = [p, u64, ctypes.c_double, p, u64, ctypes.POINTER(u64), p, ctypes.POINTER(i64), ctypes.c_int]
+        L.gzo_decompress.restype = ctypes.c_int
+        L.gzo_decompress.argtypes = [p, u64, p, u64, ctypes.POINTER(u64), ctypes.c_char_p, ctypes.c_int, ctypes.c_int]
+        L.gzo_parse_header.restype = ctypes.c_int
+        L.gzo_parse_header.argtypes = [p, u64, ctypes.POINTER(u64), ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, ctypes.c_int]
+        _lib = L
+    return _lib
+
+
+def compress_bound(n: int) -> int:
+    return int(lib().gzo_compress_bound(n))
+
+
+def compress(data, eb: float, threads: int = 1, return_offsets: bool = False):
+    """codec.compress (codec.py:149-270) -> bytes [, block offsets (codec.py:241-243)]."""
+    x = np.ascontiguousarray(data, dtype="<f4").reshape(-1)
+    n = x.size
+    cap = compress_bound(n)
+    out = np.empty(cap, dtype=np.uint8)
+    out_len = ctypes.c_uint64(0)
+    bad = ctypes.c_int64(-1)
+    nb = -(-n // BLOCK)
+    offs = np.empty(max(nb, 1), dtype=np.uint64) if return_offsets else None
+    rc = lib().gzo_compress(
+        x.ctypes.data, n, float(eb), out.ctypes.data, cap, ctypes.byref(out_len),
+        offs.ctypes.data if offs is not None else None, ctypes.byref(bad), int(threads))
+    if rc == -1:
+        raise ValueError(f"error bound must be positive and finite, got {float(eb)!r}")
+    if rc == -2:
+        raise ValueError(f"non-finite value at offset {bad.value}")
+    if rc != 0:
+        raise RuntimeError(f"oracle compress failed rc={rc}")
+    blob = out[: out_len.value].tobytes()
+    if return_offsets:
+        return blob, offs[:nb].astype(np.int64)
+    return blob
+
+
+def decompress(blob, threads: int = 1) -> np.ndarray:
+    """codec.decompress (codec.py:284-369)."""
+    b = np.frombuffer(bytes(blob), dtype=np.uint8)
+    msg = ctypes.create_string_buffer(256)
+    n = ctypes.c_uint64(0)
+    ebv = ctypes.c_double(0)
+    rc = lib().gzo_parse_header(b.ctypes.data, b.size, ctypes.byref(n), ctypes.byref(ebv), msg, 256)
+    if rc:
+        raise OracleDecodeError(msg.value.decode())
+    y = np.empty(max(n.value, 1), dtype=np.float32)
+    rc = lib().gzo_decompress(b.ctypes.data, b.size, y.ctypes.data, y.size, ctypes.byref(n), msg, 256, int(threads))
+    if rc:
+        raise OracleDecodeError(msg.value.decode())
+    return y[: n.value].copy()
+
+
+# ---------------------------------------------------------------------------
+# collective schedules (collectives.py), all ranks in one process
+# ---------------------------------------------------------------------------
+
+
+def chunk_spans(n: int, ranks: int):
+    """collectives.py:42-45."""
+    step = -(-n // ranks) if n else 0
+    return [(min(c * step, n), min((c + 1) * step, n)) for c in range(ranks)]
+
+
+def apply_op(op: str, local: np.ndarray, received: np.ndarray) -> np.ndarray:
+    """collectives.py:32-39."""
+    if op == "sum":
+        return local + received
+    if op == "max":
+        return np.maximum(local, received)
+    raise ValueError(op)
+
+
+@dataclass
+class Trace:
+    """(step, src, dst, payload) per message, like Network(record_payloads=True)."""
+
+    msgs: list
+
+
+def ring_reduce_scatter(bufs, eb, op="sum", trace=None, raw=False):
+    """ring_reduce_scatter_c, collectives.py:258-291 (two-pass schedule)."""
+    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb))
+    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else decompress
+    bufs = [np.ascontiguousarray(b, "<f4") for b in bufs]
+    N = len(bufs)
+    n = bufs[0].size
+    spans = chunk_spans(n, N)
+    acc = [[b[lo:hi].copy() for lo, hi in spans] for b in bufs]
+    if N == 1:
+        return [bufs[0].copy()]
+    for s in range(N - 1):
+        sent = []
+        for i in range(N):
+            blob = enc(acc[i][(i - s) % N])
+            sent.append(blob)
+            if trace is not None:
+                trace.append(("rs", s, i, (i + 1) % N, blob))
+        for i in range(N):
+            blob = sent[(i - 1) % N]
+            c_in = (i - s - 1) % N
+            acc[i][c_in] = apply_op(op, acc[i][c_in], dec(blob))
+    return [acc[i][(i + 1) % N] for i in range(N)]
+
+
+def ring_allgather_owned(owned, eb, chunk_of, trace=None, raw=False):
+    """_ring_allgather, collectives.py:215-244: compress once, forward bytes."""
+    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb))
+    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else decompress
+    N = len(owned)
+    gathered = [{chunk_of(i): owned[i]} for i in range(N)]
+    if N == 1:
+        return gathered
+    carry = [enc(owned[i]) for i in range(N)]  # s == 0 encodes once (227)
+    for s in range(N - 1):
+        if trace is not None:
+            for i in range(N):
+                trace.append(("ag", s, i, (i + 1) % N, carry[i]))
+        new = [carry[(i - 1) % N] for i in range(N)]
+        for i in range(N):
+            gathered[i][chunk_of((i - 1 - s) % N)] = dec(new[i])
+        carry = new
+    return gathered
+
+
+def ring_allreduce(bufs, eb, op="sum", trace=None, raw=False):
+    """ring_allreduce_c, collectives.py:294-308."""
+    bufs = [np.ascontiguousarray(b, "<f4") for b in bufs]
+    N = len(bufs)
+    if N == 1:
+        return [bufs[0].copy()]
+    owned = ring_reduce_scatter(bufs, eb, op, trace, raw)
+    gathered = ring_allgather_owned(owned, eb, lambda i: (i + 1) % N, trace, raw)
+    return [np.concatenate([gathered[i][c] for c in range(N)]) for i in range(N)]
+
+
+def ring_allgather(chunks, eb, trace=None, raw=False):
+    """ring_allgather_c, collectives.py:247-255."""
+    owned = [np.ascontiguousarray(c, "<f4") for c in chunks]
+    N = len(owned)
+    g = ring_allgather_owned(owned, eb, lambda i: i, trace, raw)
+    return [np.concatenate([g[i][c] for c in range(N)]) if N > 1 else owned[i].copy() for i in range(N)]
+
+
+def scatter_children(vr: int, size: int):
+    """_scatter_children, collectives.py:449-464."""
+    mask = 1
+    while mask < size:
+        if vr & mask:
+            break
+        mask <<= 1
+    extent = mask
+    sends = []
+    mask >>= 1
+    while mask:
+        child = vr + mask
+        if child < size:
+            sends.append((child, child, min(child + mask, size)))
+        mask >>= 1
+    return extent, sends
+
+
+def pack_scatter_msg(sizes, lo, hi, frag: bytes) -> bytes:
+    """_pack_scatter_msg, collectives.py:432-434."""
+    return _SC_HDR.pack(len(sizes), lo, hi) + np.asarray(sizes, dtype="<u8").tobytes() + frag
+
+
+def binomial_scatter(data, N, eb, root=0, counts=None, trace=None):
+    """binomial_scatter_c, collectives.py:467-532 (messages appended to trace)."""
+    data = np.ascontiguousarray(data, "<f4").reshape(-1)
+    if counts is None:
+        counts = [hi - lo for lo, hi in chunk_spans(data.size, N)]
+    counts = [int(c) for c in counts]
+    if len(counts) != N or any(c < 0 for c in counts) or sum(counts) != data.size:
+        raise ValueError("bad counts")
+    rank_lo = np.concatenate([[0], np.cumsum(counts)]).astype(int)
+    slices = [data[rank_lo[i] : rank_lo[i + 1]] for i in range(N)]
+    outputs = [None] * N
+    outputs[root] = slices[root].copy()
+    if N == 1:
+        return outputs
+    order = [(root + j) % N for j in range(N)]
+    blobs = [compress(slices[r], eb) for r in order]
+    sizes = [len(b) for b in blobs]
+    offs = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
+    payload = b"".join(blobs)
+    inbox = {}
+    _, root_sends = scatter_children(0, N)
+    for child, lo, hi in root_sends:
+        msg = pack_scatter_msg(sizes, lo, hi, payload[offs[lo] : offs[hi - 1] + sizes[hi - 1]])
+        inbox[order[child]] = msg
+        if trace is not None:
+            trace.append((root, order[child], msg))
+    for vr in range(1, N):
+        me = order[vr]
+        _, sends = scatter_children(vr, N)
+        msg = inbox[me]
+        cnt, lo, hi = _SC_HDR.unpack_from(msg)
+        frag = msg[_SC_HDR.size + 8 * cnt :]
+        for child, clo, chi in sends:
+            sub = frag[offs[clo] - offs[lo] : offs[chi - 1] + sizes[chi - 1] - offs[lo]]
+            cmsg = pack_scatter_msg(sizes, clo, chi, sub)
+            inbox[order[child]] = cmsg
+            if trace is not None:
+                trace.append((me, order[child], cmsg))
+        own = frag[offs[vr] - offs[lo] : offs[vr] + sizes[vr] - offs[lo]]
+        outputs[me] = decompress(own)
+    return outputs
+
+
+def smooth_field(n: int, phase: float = 0.0) -> np.ndarray:
+    """SURVEY §8(d) cfg1/cfg2 field: f32(0.5 sin(2πi/65536 + φ) + 0.25 sin(2πi/4099 + φ))."""
+    i = np.arange(n, dtype=np.float64)
+    return (0.5 * np.sin(2 * np.pi * i / 65536 + phase) + 0.25 * np.sin(2 * np.pi * i / 4099 + phase)).astype(np.float32)
