@@ -1,0 +1,122 @@
+/*
+ * gzccl.h -- C ABI of the B200-native gZCCL hot path (libgzccl.so, sm_100a).
+ *
+ * Plain pointers and sizes only; every pointer is device memory unless stated.
+ * The reference (/root/reference/pkg/src/gzccl) is a Python package with no
+ * native layer, so each entry point names the Python interface it replaces;
+ * the Python shim paper_2308_05199_b200/ binds these through ctypes with the
+ * reference's names and error behaviour.
+ *
+ * Conventions
+ *   - Return value: 0 on success, otherwise a cudaError_t (launch/driver
+ *     errors) or one of the GZ_E* codes below (argument errors).
+ *   - Data-dependent errors (non-finite input, malformed blob) are written by
+ *     the kernels into a caller-owned device gz_status that the caller resets
+ *     with gz_status_reset() and inspects after synchronising.
+ *   - Every call is stream-ordered on `stream` and never allocates.
+ *   - A workspace (gz_workspace_bytes) must be zeroed once with
+ *     gz_workspace_init(); it may then be reused by any number of calls that
+ *     are ordered on one stream (one workspace per concurrent stream).
+ */
+#ifndef GZCCL_H
+#define GZCCL_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* gz_stream_t; /* == cudaStream_t */
+
+enum {
+  GZ_OK = 0,
+  GZ_EINVAL = 10001,    /* bad argument: null pointer, size, alignment */
+  GZ_EBOUND = 10002,    /* error bound not finite and > 0 (codec.py:89-93) */
+  GZ_ECAPACITY = 10003, /* output buffer smaller than gz_compress_bound(n) */
+  GZ_EBLOCK = 10004     /* block size other than 32 (format is frozen, codec.py:42) */
+};
+
+/* Device error record (32 bytes). */
+typedef struct gz_status {
+  uint64_t first_nonfinite; /* index of the first non-finite input, ~0 if none (codec.py:83-85) */
+  uint64_t decode_error;    /* (block_index << 8) | code, ~0 if none; codes 1 width, 2 truncated,
+                               3 trailing bytes, 4 sidecar mismatch, 5 header (codec.py:273-322) */
+  uint64_t reserved[2];
+} gz_status;
+
+/* ---- sizing (host functions, no device work) ---------------------------- */
+/* Compressed-size bound incl. header and 64 B of read slack.  Tighter than
+ * worst_case_blob_bytes (codec.py:492-494): raw blocks are 129 B, not 133. */
+uint64_t gz_compress_bound(uint64_t n);
+uint64_t gz_num_tiles(uint64_t n);        /* tiles of GZ_TILE_BLOCKS blocks */
+uint32_t gz_tile_blocks(void);            /* 32-value blocks per tile (CTA) */
+uint64_t gz_sidecar_bytes(uint64_t n);    /* u64 tile offsets + u16 group offsets */
+uint64_t gz_workspace_bytes(uint64_t n);  /* tile status words for the look-back */
+
+/* ---- setup ---------------------------------------------------------------- */
+int gz_workspace_init(void* ws, uint64_t ws_bytes, gz_stream_t stream);
+int gz_status_reset(gz_status* d_status, gz_stream_t stream);
+
+/* ---- codec ------------------------------------------------------------------
+ * gz_compress replaces codec.compress(data, eb, workspace) (codec.py:149-270).
+ *   x[n] f32 -> blob (reference byte format, header included) of length
+ *   *d_len; blob_cap >= gz_compress_bound(n); blob 16-byte aligned.
+ *   sidecar (gz_sidecar_bytes, may be NULL): tile/group offsets for decoders.
+ *   d_block_offsets (nb = ceil(n/32) u64, may be NULL): payload offset of
+ *   every block == np.cumsum(sizes) exclusive scan (codec.py:241-243).
+ *   block must be 32.
+ */
+int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* blob, uint64_t blob_cap,
+                uint64_t* d_len, void* sidecar, uint64_t* d_block_offsets, void* ws, uint64_t ws_bytes,
+                gz_status* d_status, gz_stream_t stream);
+
+/* gz_decompress_sidecar replaces codec.decompress(blob) (codec.py:284-369)
+ * when the blob's sidecar is available (collective path).  n and eb are the
+ * blob header's values; y[n] f32 output. */
+int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, double eb, float* y,
+                          gz_status* d_status, gz_stream_t stream);
+
+/* gz_index replaces the sequential block walk of codec.decompress
+ * (codec.py:298-322): validates the payload of a blob of header count n and
+ * payload length payload_len (device pointer to the blob) and builds its
+ * sidecar, so that any reference-produced blob can be decoded on the device.
+ * Errors are reported in d_status->decode_error with the reference's
+ * semantics (first failing block in walk order). */
+int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sidecar, void* ws, uint64_t ws_bytes,
+             gz_status* d_status, gz_stream_t stream);
+uint64_t gz_index_workspace_bytes(uint64_t payload_len);
+
+/* ---- fused ring reduce-scatter step ----------------------------------------
+ * One step of ring_reduce_scatter_c (collectives.py:274-290) for one rank:
+ *   acc = op(local, decompress(blob_in))   (op 0 = sum "+", 1 = np.maximum)
+ *   blob_out = compress(acc, eb)           (sidecar_out written alongside)
+ *   acc_out[m] (may be NULL) receives acc.
+ * blob_out / sidecar_out / d_len_out may point into a peer GPU's memory
+ * (CUDA IPC over NVLink): the step then also performs the send. */
+int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* local, uint64_t m, double eb,
+                   int op, float* acc_out, uint8_t* blob_out, uint64_t blob_out_cap, uint64_t* d_len_out,
+                   void* sidecar_out, void* ws, uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream);
+
+/* ---- multi-segment compression (binomial scatter root) ----------------------
+ * compress_blocks (codec.py:408-427): nseg independent blobs, blob i written
+ * at payload + seg_blob_off[i] (host-planned worst-case slots). */
+int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,
+                         const uint64_t* h_seg_blob_off, uint64_t* d_seg_len, void* sidecars,
+                         const uint64_t* h_seg_sidecar_off, void* ws, uint64_t ws_bytes, gz_status* d_status,
+                         gz_stream_t stream);
+
+/* ---- peer memory (CUDA IPC over NVLink) ----------------------------------- */
+int gz_ipc_handle_size(void);
+int gz_ipc_get_handle(void* dptr, void* handle_out /* gz_ipc_handle_size() bytes */);
+int gz_ipc_open_handle(const void* handle, void** dptr_out);
+int gz_ipc_close(void* dptr);
+int gz_enable_peer_access(int peer_device);
+/* stream-ordered flags (driver stream memory ops; no spinning kernels) */
+int gz_stream_write_u32(gz_stream_t stream, void* dptr, uint32_t value);
+int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value);
+/* copy `*d_len + tail` bytes determined on the device: dst may be a peer */
+int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64_t max_bytes, gz_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

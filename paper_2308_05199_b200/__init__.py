@@ -1,0 +1,44 @@
+"""B200-native gZCCL: error-bounded compression and compression-enabled collectives.
+
+Drop-in for the hot path of the reference ``gzccl`` package
+(/root/reference/pkg/src/gzccl): the codec API (``compress`` /
+``decompress`` / ``compress_blocks`` / ``decompress_block``, same byte format)
+and the compressed ring Allreduce / binomial Scatter, running as hand-written
+sm_100a kernels (``libgzccl.so``) over NVLink peer memory.
+"""
+
+from .codec import (
+    BLOCK,
+    HEADER_BYTES,
+    MAGIC,
+    MAX_STEP,
+    RAW_WIDTH,
+    BlockTable,
+    DecodeError,
+    DeviceBlob,
+    Workspace,
+    compress,
+    compress_blocks,
+    decompress,
+    decompress_block,
+    worst_case_blob_bytes,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BLOCK",
+    "HEADER_BYTES",
+    "MAGIC",
+    "MAX_STEP",
+    "RAW_WIDTH",
+    "BlockTable",
+    "DecodeError",
+    "DeviceBlob",
+    "Workspace",
+    "compress",
+    "compress_blocks",
+    "decompress",
+    "decompress_block",
+    "worst_case_blob_bytes",
+]

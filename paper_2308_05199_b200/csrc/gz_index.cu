@@ -1,0 +1,193 @@
+// gz_index.cu -- device replacement for the sequential block walk of
+// codec.decompress (codec.py:298-322): validate a reference blob's payload and
+// build the tile/group sidecar the tile decoder needs.
+//
+// A block's size is a function of its first byte, so block starts form a
+// chain.  The payload is cut into SEG-byte segments; the first block start in
+// any segment lies in its first 129 bytes (a block is at most 129 bytes).
+//   K1 idx_segments : for every segment and each of the 129 possible entry
+//                     offsets, walk the chain to the segment's end (one thread
+//                     per entry) -> exit offset + number of block starts.
+//   K2 idx_chunks   : compose CH consecutive segment maps (shared memory).
+//   K3 idx_resolve  : follow the composed maps from entry 0 (one thread,
+//                     one lookup per chunk) -> actual entry + block base.
+//   K4 idx_emit     : per chunk, derive each segment's actual entry, re-walk
+//                     the true chain with true block indices, apply the
+//                     reference's checks in walk order (first failing block
+//                     wins), and record the start of every 32nd block.
+//   K5 idx_sidecar  : convert those starts into the sidecar layout.
+#include "gz_device.cuh"
+
+namespace gz {
+
+constexpr int SEG = 2048;
+constexpr int NE = 129;       // possible entry offsets
+constexpr int CH = 128;       // segments per chunk
+constexpr short EX_DEAD = -1;  // invalid width byte on the chain
+constexpr short EX_END = -2;   // chain reached the payload end inside the segment
+
+struct IndexWs {
+  short* exit;            // [nseg][NE]
+  unsigned short* count;  // [nseg][NE]
+  short* cexit;           // [nchunk][NE]
+  unsigned* ccount;       // [nchunk][NE]
+  long long* centry;      // [nchunk] actual entry (offset in first segment), <0 if unreachable
+  unsigned long long* cbase;  // [nchunk] block index of the first start in the chunk
+  unsigned long long* g32;    // [ceil(nb/32)] payload offset of block 32k
+};
+
+__device__ __forceinline__ int full_size(int w) { return w == RAW_WIDTH ? 1 + 4 * BLOCK : 5 + (31 * w + 7) / 8; }
+
+__global__ void __launch_bounds__(160) idx_segments(const uint8_t* payload, uint64_t psize, IndexWs ws) {
+  __shared__ uint8_t seg[SEG];
+  const uint64_t s = blockIdx.x;
+  const uint64_t g0 = s * SEG;
+  const int len = (int)umin64(SEG, psize - g0);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) seg[i] = __ldg(payload + g0 + i);
+  __syncthreads();
+  const int e = threadIdx.x;
+  if (e >= NE) return;
+  int p = e, cnt = 0;
+  short ex;
+  while (true) {
+    if (p >= SEG) {
+      ex = (short)(p - SEG);
+      break;
+    }
+    if (p >= len) {  // the payload ends inside this segment
+      ex = EX_END;
+      break;
+    }
+    const int w = seg[p];
+    if (w > 32 && w != RAW_WIDTH) {
+      ex = EX_DEAD;
+      break;
+    }
+    p += full_size(w);
+    ++cnt;
+  }
+  ws.exit[s * NE + e] = ex;
+  ws.count[s * NE + e] = (unsigned short)cnt;
+}
+
+__global__ void __launch_bounds__(160) idx_chunks(uint64_t nseg, IndexWs ws) {
+  extern __shared__ unsigned char sm[];
+  short* sx = reinterpret_cast<short*>(sm);
+  unsigned short* sc = reinterpret_cast<unsigned short*>(sm + CH * NE * sizeof(short));
+  const uint64_t c = blockIdx.x;
+  const uint64_t s0 = c * CH;
+  const int ns = (int)umin64(CH, nseg - s0);
+  for (int i = threadIdx.x; i < ns * NE; i += blockDim.x) {
+    sx[i] = ws.exit[s0 * NE + i];
+    sc[i] = ws.count[s0 * NE + i];
+  }
+  __syncthreads();
+  const int e = threadIdx.x;
+  if (e >= NE) return;
+  int cur = e;
+  unsigned tot = 0;
+  for (int k = 0; k < ns && cur >= 0; ++k) {
+    tot += sc[k * NE + cur];
+    cur = sx[k * NE + cur];
+  }
+  ws.cexit[c * NE + e] = (short)cur;
+  ws.ccount[c * NE + e] = tot;
+}
+
+__global__ void idx_resolve(uint64_t nchunk, IndexWs ws) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  long long entry = 0;
+  unsigned long long base = 0;
+  for (uint64_t c = 0; c < nchunk; ++c) {
+    ws.centry[c] = entry;
+    ws.cbase[c] = base;
+    if (entry < 0) continue;
+    base += ws.ccount[c * NE + entry];
+    entry = ws.cexit[c * NE + entry];
+  }
+}
+
+// record (block << 24) | (w << 8) | code, the smallest block wins
+__device__ __forceinline__ void idx_error(Status* st, uint64_t blk, int w, unsigned code) {
+  atomicMin(&st->decode_error, (unsigned long long)((blk << 24) | ((uint64_t)(w & 0xFFFF) << 8) | code));
+}
+
+__global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t psize, uint64_t nseg, uint64_t n,
+                                               IndexWs ws, Status* st) {
+  __shared__ int s_entry[CH];
+  __shared__ unsigned long long s_base[CH];
+  const uint64_t c = blockIdx.x;
+  const uint64_t s0 = c * CH;
+  const int ns = (int)umin64(CH, nseg - s0);
+  const uint64_t nb = (n + BLOCK - 1) / BLOCK;
+  const int last_cnt = (int)(n - (nb - 1) * BLOCK);
+  if (threadIdx.x == 0) {
+    long long entry = ws.centry[c];
+    unsigned long long base = ws.cbase[c];
+    for (int k = 0; k < ns; ++k) {
+      s_entry[k] = (int)entry;
+      s_base[k] = base;
+      if (entry >= 0) {
+        base += ws.count[(s0 + k) * NE + entry];
+        entry = ws.exit[(s0 + k) * NE + entry];
+      }
+    }
+  }
+  __syncthreads();
+  const int k = threadIdx.x;
+  if (k >= ns) return;
+  const uint64_t s = s0 + k;
+  int e = s_entry[k];
+  if (e == EX_END || e == EX_DEAD || e < 0) {
+    // chain never enters this segment: an earlier segment reported the error
+    // (or the true chain ended before this segment)
+    return;
+  }
+  uint64_t pos = s * SEG + (uint64_t)e;
+  uint64_t blk = s_base[k];
+  const uint64_t send = (s + 1) * SEG;
+  while (pos < send && blk < nb) {
+    if (pos >= psize) {  // codec.py:307-308
+      idx_error(st, blk, 0, DE_TRUNC);
+      return;
+    }
+    const int w = __ldg(payload + pos);
+    const int cnt = (blk == nb - 1) ? last_cnt : BLOCK;
+    int size;
+    if (w == RAW_WIDTH) size = 1 + 4 * cnt;  // 310-311
+    else if (w <= 32) size = 5 + ((cnt - 1) * w + 7) / 8;  // 312-313
+    else {  // 314-315
+      idx_error(st, blk, w, DE_WIDTH);
+      return;
+    }
+    if ((blk & 31) == 0) ws.g32[blk >> 5] = pos;
+    pos += size;
+    if (pos > psize) {  // 319-320
+      idx_error(st, blk, 0, DE_TRUNC);
+      return;
+    }
+    if (blk == nb - 1 && pos != psize) {  // 321-322
+      idx_error(st, nb, 0, DE_TRAIL);
+      st->pad[0] = psize - pos;
+      return;
+    }
+    ++blk;
+  }
+  // the chain ran out of payload inside this segment before nb blocks
+  if (blk < nb && pos >= psize && pos < send) idx_error(st, blk, 0, DE_TRUNC);
+}
+
+__global__ void idx_sidecar(const IndexWs ws, uint64_t n, uint64_t psize, uint64_t* tile_off, uint16_t* sub_off) {
+  const uint64_t nb = (n + BLOCK - 1) / BLOCK;
+  const uint64_t ntiles = (nb + TB - 1) / TB;
+  const uint64_t ng = (nb + 31) / 32;
+  const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (i < ntiles) tile_off[i] = ws.g32[i * GROUPS];
+  if (i == ntiles) tile_off[ntiles] = psize;
+  if (i < ntiles * GROUPS) {
+    const uint64_t t = i / GROUPS;
+    sub_off[i] = (uint16_t)(i < ng ? ws.g32[i] - ws.g32[t * GROUPS] : 0);
+  }
+}
+
+}  // namespace gz

@@ -1,0 +1,175 @@
+"""Device codec parity: libgzccl.so kernels vs the reference (golden fixtures)
+and vs the CPU oracle on seeded inputs.  Bit-exact bytes, offsets, outputs."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+import golden_data as G
+from conftest import max_err
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2308_05199_b200 as gz  # noqa: E402
+
+CASES = G.codec_cases()
+
+
+@pytest.fixture(scope="module")
+def ws():
+    return gz.Workspace()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_compress_bytes_and_offsets_match_reference(case, ws):
+    x = torch.from_numpy(case.x).cuda()
+    blob = gz.compress(x, case.eb, ws, return_offsets=True)
+    assert bytes(blob) == case.blob
+    if case.x.size:
+        assert np.array_equal(blob.block_offsets.cpu().numpy(), case.block_offsets)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_decompress_sidecar_matches_reference(case, ws):
+    blob = gz.compress(torch.from_numpy(case.x).cuda(), case.eb, ws)
+    y = gz.decompress(blob, ws)
+    assert y.cpu().numpy().tobytes() == case.y.tobytes()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_decompress_reference_blob(case, ws):
+    # a blob produced by the reference, decoded on the device (gz_index path)
+    y = gz.decompress(case.blob, ws)
+    assert isinstance(y, np.ndarray)
+    assert y.tobytes() == case.y.tobytes()
+
+
+def test_host_api_returns_bytes(ws):
+    data, eb = G.golden_data(2)
+    out = gz.compress(data, eb)
+    assert isinstance(out, bytes) and out == G.golden_blob(2)
+    back = gz.decompress(out)
+    assert isinstance(back, np.ndarray) and max_err(data, back) <= eb
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_vs_oracle(seed, oracle, ws):
+    rng = np.random.default_rng(seed)
+    for _ in range(6):
+        n = int(rng.integers(1, 300_000))
+        kind = rng.integers(0, 4)
+        if kind == 0:
+            x = rng.uniform(-1, 1, n).astype(np.float32)
+        elif kind == 1:
+            x = np.cumsum(rng.normal(0, 1e-3, n)).astype(np.float32)
+        elif kind == 2:
+            x = (rng.uniform(-1, 1, n) * 10.0 ** rng.integers(-6, 6, n)).astype(np.float32)
+        else:
+            x = oracle.smooth_field(n, float(seed))
+        eb = float(rng.choice([1e-2, 1e-3, 1e-4, 1e-5, 1e-6, 3.7e-4]))
+        ref = oracle.compress(x, eb, threads=8)
+        blob = gz.compress(torch.from_numpy(x).cuda(), eb, ws)
+        assert bytes(blob) == ref
+        assert gz.decompress(blob, ws).cpu().numpy().tobytes() == oracle.decompress(ref, threads=8).tobytes()
+
+
+@pytest.mark.parametrize("eb", [1e-4, 1e-3, 1e-2])
+def test_cfg1_field_bit_exact(eb, oracle, ws):
+    n = 1 << 24
+    x = oracle.smooth_field(n)
+    ref, offs = oracle.compress(x, eb, threads=8, return_offsets=True)
+    blob = gz.compress(torch.from_numpy(x).cuda(), eb, ws, return_offsets=True)
+    assert len(blob) == len(ref)
+    assert bytes(blob) == ref
+    assert np.array_equal(blob.block_offsets.cpu().numpy(), offs)
+    d = G.digests()
+    if hashlib.sha256(x.tobytes()).hexdigest() == d["cfg1_input_sha256"]:
+        assert hashlib.sha256(ref).hexdigest() == d[f"cfg1_eb{eb!r}"]["sha256"]
+    y = gz.decompress(blob, ws).cpu().numpy()
+    assert y.tobytes() == oracle.decompress(ref, threads=8).tobytes()
+    assert max_err(x, y) <= eb
+
+
+def test_unaligned_and_offset_views(oracle, ws):
+    base = torch.from_numpy(oracle.smooth_field(100_003)).cuda()
+    for off in (1, 2, 3, 5, 31, 33):
+        v = base[off:]
+        assert bytes(gz.compress(v, 1e-4, ws)) == oracle.compress(base[off:].cpu().numpy(), 1e-4)
+
+
+def test_errors(ws):
+    with pytest.raises(ValueError, match="offset 2"):
+        gz.compress(torch.tensor([0.0, 1.0, float("nan")], device="cuda"), 1e-4, ws)
+    with pytest.raises(ValueError, match="offset 0"):
+        gz.compress(np.array([np.inf], np.float32), 1e-4)
+    x = np.zeros(100, np.float32)
+    x[77] = -np.inf
+    with pytest.raises(ValueError, match="offset 77"):
+        gz.compress(x, 1e-4)
+    for eb in (0.0, -1e-4, float("nan"), float("inf")):
+        with pytest.raises(ValueError):
+            gz.compress(np.ones(4, np.float32), eb)
+    with pytest.raises(ValueError):
+        gz.compress(np.ones(64, np.float32), 1e-4, block=64)
+    blob = gz.compress(np.zeros(64, np.float32), 1e-4)
+    with pytest.raises(gz.DecodeError, match="trailing"):
+        gz.decompress(blob + b"\x00")
+    bad = bytearray(blob)
+    bad[24] = 77
+    with pytest.raises(gz.DecodeError, match="width"):
+        gz.decompress(bytes(bad))
+    with pytest.raises(gz.DecodeError, match="magic"):
+        gz.decompress(b"XXXX" + blob[4:])
+    with pytest.raises(gz.DecodeError):
+        gz.decompress(b"GZC1\x00\x00")
+    b2 = gz.compress(np.random.default_rng(0).uniform(0, 1, 100).astype(np.float32), 1e-4)
+    with pytest.raises(gz.DecodeError, match="truncated"):
+        gz.decompress(b2[:-3])
+
+
+def test_compress_blocks_and_decompress_block(ws):
+    rng = np.random.default_rng(3)
+    counts = [100, 2000, 4, 1992, 0]
+    data = rng.uniform(0, 1, sum(counts)).astype(np.float32)
+    payload, table = gz.compress_blocks(data, counts, 1e-4)
+    import oracle.oracle as O
+
+    expect = b"".join(O.compress(data[sum(counts[:i]) : sum(counts[: i + 1])], 1e-4) for i in range(len(counts)))
+    assert payload == expect
+    assert table.sizes[4] == 24
+    pos = 0
+    for i, c in enumerate(counts):
+        got = gz.decompress_block(payload, table, i)
+        assert got.size == c
+        assert max_err(data[pos : pos + c], got) <= 1e-4
+        pos += c
+    with pytest.raises(IndexError):
+        gz.decompress_block(payload, table, 5)
+    with pytest.raises(ValueError, match="sum"):
+        gz.compress_blocks(np.zeros(10, np.float32), [4, 4], 1e-4)
+    with pytest.raises(ValueError, match="chain"):
+        gz.BlockTable(sizes=(3, 4), offsets=(0, 5))
+
+
+def test_many_segments_one_launch(oracle, ws):
+    rng = np.random.default_rng(11)
+    counts = [int(c) for c in rng.integers(0, 20000, 70)]
+    data = oracle.smooth_field(sum(counts), 0.3)
+    payload, table = gz.compress_blocks(data, counts, 1e-3)
+    pos = 0
+    for i, c in enumerate(counts):
+        assert payload[table.offsets[i] : table.offsets[i] + table.sizes[i]] == oracle.compress(data[pos : pos + c], 1e-3)
+        pos += c
+
+
+def test_workspace_reuse_and_determinism(ws, oracle):
+    x = torch.from_numpy(oracle.smooth_field(777_777)).cuda()
+    a = bytes(gz.compress(x, 1e-4, ws))
+    for _ in range(5):
+        assert bytes(gz.compress(x, 1e-4, ws)) == a
+    assert bytes(gz.compress(x, 1e-4, gz.Workspace())) == a

@@ -1,0 +1,100 @@
+"""Collective schedules with N virtual ranks on one GPU vs the reference's own
+outputs and traced messages (golden fixtures) -- bit-exact."""
+
+import numpy as np
+import pytest
+
+import golden_data as G
+from conftest import max_err
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2308_05199_b200 as gz  # noqa: E402
+from paper_2308_05199_b200 import collectives as C  # noqa: E402
+
+RING = G.ring_cases()
+
+
+@pytest.fixture(scope="module")
+def ws():
+    return gz.Workspace()
+
+
+@pytest.mark.parametrize("case", RING, ids=[f"{c.algo}-N{c.N}-n{c.n}-{c.op}" for c in RING])
+def test_ring_matches_reference(case, ws):
+    outs, rep = C.run_collective(case.algo, case.inputs, eb=case.eb, reduce_op=case.op, record_payloads=True,
+                                 workspace=ws)
+    assert len(outs) == case.N
+    for o, e in zip(outs, case.outputs):
+        assert o.cpu().numpy().tobytes() == e.tobytes()
+    msgs = rep.trace.msgs
+    assert [m[2] for m in msgs] == case.msgs
+    assert [m[0] for m in msgs] == list(case.src) and [m[1] for m in msgs] == list(case.dst)
+
+
+SCAT = G.scatter_cases()
+
+
+@pytest.mark.parametrize("case", SCAT, ids=[f"N{c.N}-root{c.root}" for c in SCAT])
+def test_scatter_matches_reference(case, ws):
+    outs, rep = C.run_collective("binomial-scatter", case.data, ranks=case.N, eb=1e-4, counts=case.counts,
+                                 root=case.root, record_payloads=True, workspace=ws)
+    for o, e in zip(outs, case.outputs):
+        assert o.cpu().numpy().tobytes() == e.tobytes()
+    assert [m[2] for m in rep.trace.msgs] == case.msgs
+    assert [m[0] for m in rep.trace.msgs] == list(case.src)
+    assert [m[1] for m in rep.trace.msgs] == list(case.dst)
+
+
+OP_COUNT_CASES = [
+    ("ring-reduce-scatter", lambda N: (N - 1, N - 1)),
+    ("ring-allgather", lambda N: (1, N - 1)),
+    ("ring-allreduce", lambda N: (N, 2 * (N - 1))),
+]
+
+
+@pytest.mark.parametrize("N", [2, 3, 4, 8])
+@pytest.mark.parametrize("algo,expect", OP_COUNT_CASES)
+def test_op_counts(algo, expect, N, ws):
+    # pkg/tests/test_collectives.py:61-80
+    rng = np.random.default_rng(N)
+    inputs = [rng.uniform(0, 1, 2 * N).astype(np.float32) for _ in range(N)]
+    _, rep = C.run_collective(algo, inputs, eb=1e-4, workspace=ws)
+    for c in rep.counters_per_rank:
+        assert (c["n_compress"], c["n_decompress"]) == expect(N)
+
+
+@pytest.mark.parametrize("eb", [1e-3, 1e-4, 1e-5])
+@pytest.mark.parametrize("N", [2, 4, 8])
+def test_allreduce_error_budget(eb, N, oracle, ws):
+    # README error budgets: ring allreduce <= N * eb vs the lossless ring
+    rng = np.random.default_rng(int(N / eb) % 1000)
+    n = 50_000
+    inputs = [oracle.smooth_field(n, 0.37 * r) + rng.normal(0, 1e-2, n).astype(np.float32) for r in range(N)]
+    outs, _ = C.run_collective("ring-allreduce", inputs, eb=eb, workspace=ws)
+    lossless = oracle.ring_allreduce(inputs, eb, raw=True)
+    for o, e in zip(outs, lossless):
+        assert max_err(e, o.cpu().numpy()) <= N * eb
+
+
+def test_errors(ws):
+    with pytest.raises(ValueError, match="equal length"):
+        C.run_collective("ring-allreduce", [np.zeros(10, np.float32), np.zeros(11, np.float32)], eb=1e-4, workspace=ws)
+    with pytest.raises(ValueError, match="counts"):
+        C.run_collective("binomial-scatter", np.zeros(10, np.float32), ranks=2, eb=1e-4, counts=[4, 4], workspace=ws)
+    with pytest.raises(ValueError, match="unknown algorithm"):
+        C.run_collective("nope", [np.zeros(4, np.float32)], eb=1e-4)
+    with pytest.raises(ValueError, match="unknown reduce op"):
+        C.run_collective("ring-allreduce", [np.zeros(4, np.float32)] * 2, eb=1e-4, reduce_op="prod", workspace=ws)
+
+
+def test_zero_preservation(ws):
+    zeros = [np.zeros(64, np.float32) for _ in range(4)]
+    for algo in ("ring-allgather", "ring-reduce-scatter", "ring-allreduce"):
+        outs, _ = C.run_collective(algo, zeros, eb=1e-4, workspace=ws)
+        for o in outs:
+            assert torch.all(o == 0.0)
