@@ -50,7 +50,7 @@ uint64_t gz_compress_bound(uint64_t n);
 uint64_t gz_num_tiles(uint64_t n);        /* tiles of GZ_TILE_BLOCKS blocks */
 uint32_t gz_tile_blocks(void);            /* 32-value blocks per tile (CTA) */
 uint64_t gz_sidecar_bytes(uint64_t n);    /* u64 tile offsets + u16 group offsets */
-uint64_t gz_workspace_bytes(uint64_t n);  /* tile status words for the look-back */
+uint64_t gz_workspace_bytes(uint64_t n);  /* CTA status words, per-tile offsets and the L2 scratch */
 
 /* ---- setup ---------------------------------------------------------------- */
 int gz_workspace_init(void* ws, uint64_t ws_bytes, gz_stream_t stream);
@@ -99,6 +99,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
 /* ---- multi-segment compression (binomial scatter root) ----------------------
  * compress_blocks (codec.py:408-427): nseg independent blobs, blob i written
  * at payload + seg_blob_off[i] (host-planned worst-case slots). */
+uint64_t gz_segments_workspace_bytes(const uint64_t* h_counts, uint32_t nseg);
 int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,
                          const uint64_t* h_seg_blob_off, uint64_t* d_seg_len, void* sidecars,
                          const uint64_t* h_seg_sidecar_off, void* ws, uint64_t ws_bytes, gz_status* d_status,

@@ -33,6 +33,7 @@ SIGNATURES = {
     "gz_index": (i32, [p, u64, u64, p, p, u64, p, p]),
     "gz_index_workspace_bytes": (u64, [u64]),
     "gz_reduce_step": (i32, [p, p, p, u64, dbl, i32, p, p, u64, p, p, p, u64, p, p]),
+    "gz_segments_workspace_bytes": (u64, [p, u32]),
     "gz_compress_segments": (i32, [p, p, u32, dbl, p, p, p, p, p, p, u64, p, p]),
     "gz_ipc_handle_size": (i32, []),
     "gz_ipc_get_handle": (i32, [p, p]),

@@ -15,7 +15,8 @@ using namespace gz;
 
 namespace {
 
-constexpr size_t SMEM_BYTES = (size_t)TB * 128 + STAGE_BYTES;
+constexpr size_t ENC_SMEM_BYTES = (size_t)WARPS * ENC_WARP_SMEM;  // per warp: two value tiles + staging
+constexpr size_t DEC_SMEM_BYTES = (size_t)WARPS * DEC_WARP_SMEM;  // per warp: value tile + two stagings
 constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-parameter budget)
 
 inline uint64_t nblocks(uint64_t n) { return (n + BLOCK - 1) / BLOCK; }
@@ -29,14 +30,21 @@ QParams make_qparams(double eb) {
   p.eb = eb;
   p.tw = 2.0 * eb;  // codec.py:188
   p.fast = std::isfinite(p.tw) && p.tw >= std::ldexp(1.0, -100) && p.tw <= std::ldexp(1.0, 100);
+  p.rtw = 0.f;
+  p.thr = 0.f;
+  p.elo = 0.f;
+  p.ehi = 0.f;
   if (p.fast) {
     p.rtw = (float)(1.0 / p.tw);
-    p.kx = std::nextafterf((float)(std::ldexp(1.0, -23) / p.tw), INFINITY);
-    p.thr = 0.5f - 0x1p-20f - 0x1p-23f;
-  } else {
-    p.rtw = 0.f;
-    p.kx = 0.f;
-    p.thr = 0.f;
+    p.thr = 0.5f - 0x1p-20f;
+    const double lo = eb * (1.0 - std::ldexp(1.0, -22));
+    float f = (float)lo;
+    if ((double)f > lo) f = std::nextafterf(f, 0.0f);
+    p.elo = f;
+    const double hi = eb * (1.0 + std::ldexp(1.0, -22));
+    float g = (float)hi;
+    if ((double)g < hi) g = std::nextafterf(g, INFINITY);
+    p.ehi = g;
   }
   return p;
 }
@@ -56,10 +64,66 @@ SidecarView sidecar_view(const void* sc, uint64_t n) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-template <int SRC, int NSEG>
-int launch_encode(const EncodeArgs<NSEG>& a, cudaStream_t s) {
-  k_tile_encode<SRC, NSEG><<<(unsigned)a.nctas, TB, SMEM_BYTES, s>>>(a);
+// Persistent grid: as many CTAs as fit on the device at once, capped by the
+// number of tiles (each warp takes tiles in ticket order).
+template <typename K>
+int grid_cap(K kernel, size_t smem, int& cache) {
+  if (cache < 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, CTA_THREADS, smem);
+    cache = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
+  }
+  return cache;
+}
+
+struct WsView {
+  TileWs* hdr;
+  uint32_t* tile_rel;
+  uint8_t* scratch;
+};
+inline uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
+inline uint64_t ws_bytes_for_tiles(uint64_t tiles) {
+  return align16(sizeof(TileWs)) + align16(4 * tiles) + tiles * (uint64_t)TILE_SLOT + 64;
+}
+WsView carve(void* ws, uint64_t tiles) {
+  uint8_t* p = reinterpret_cast<uint8_t*>(ws);
+  WsView v;
+  v.hdr = reinterpret_cast<TileWs*>(p);
+  v.tile_rel = reinterpret_cast<uint32_t*>(p + align16(sizeof(TileWs)));
+  v.scratch = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(p + align16(sizeof(TileWs)) + align16(4 * tiles)) + 15) & ~(uintptr_t)15);
+  return v;
+}
+
+// Grid = CTAs that fit at once (capped by the work); the CTAs are split over
+// segments in proportion to their tiles (at least one CTA per segment).
+template <int SRC, int NSEG, bool FAST>
+int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
+  static int cap = -1;
+  grid_cap(k_tile_encode<SRC, NSEG, FAST>, ENC_SMEM_BYTES, cap);
+  uint64_t G = std::min<uint64_t>((uint64_t)cap, (total_tiles + WARPS - 1) / WARPS);
+  G = std::max<uint64_t>(G, (uint64_t)a.nseg);
+  uint64_t base = 0;
+  for (int k = 0; k < a.nseg; ++k) {
+    const uint64_t tk = ntiles_of(a.seg[k].n);
+    uint64_t ck = total_tiles ? (G * tk) / total_tiles : 1;
+    ck = std::max<uint64_t>(1, std::min<uint64_t>(ck, std::max<uint64_t>(1, (tk + WARPS - 1) / WARPS)));
+    a.seg[k].cta_base = base;
+    base += ck;
+  }
+  if (base > (uint64_t)MAXGRID) return GZ_EINVAL;
+  a.nctas = base;
+  k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, CTA_THREADS, ENC_SMEM_BYTES, s>>>(a);
   return (int)cudaGetLastError();
+}
+
+template <int SRC, int NSEG>
+int launch_encode(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
+  return a.qp.fast ? launch_encode_t<SRC, NSEG, true>(a, total_tiles, s)
+                   : launch_encode_t<SRC, NSEG, false>(a, total_tiles, s);
 }
 
 __global__ void k_record_error(Status* st, unsigned long long v) { atomicMin(&st->decode_error, v); }
@@ -114,7 +178,7 @@ uint64_t gz_sidecar_bytes(uint64_t n) {
   const uint64_t nt = ntiles_of(n);
   return ((8 * (nt + 1) + 2 * nt * GROUPS) + 15) & ~15ull;
 }
-uint64_t gz_workspace_bytes(uint64_t n) { return 32 + 8 * (nctas_of(n) + 1); }
+uint64_t gz_workspace_bytes(uint64_t n) { return ws_bytes_for_tiles(ntiles_of(n)); }
 
 int gz_workspace_init(void* ws, uint64_t ws_bytes, gz_stream_t stream) {
   if (!ws || ws_bytes < 40) return GZ_EINVAL;
@@ -137,14 +201,16 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0};
+  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0};
   a.nseg = 1;
-  a.nctas = nctas_of(n);
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
-  a.ws = reinterpret_cast<TileWs*>(ws);
+  const WsView wv = carve(ws, ntiles_of(n));
+  a.ws = wv.hdr;
+  a.tile_rel = wv.tile_rel;
+  a.scratch = wv.scratch;
   a.st = reinterpret_cast<Status*>(d_status);
-  return launch_encode<SRC_PLAIN, 1>(a, (cudaStream_t)stream);
+  return launch_encode<SRC_PLAIN, 1>(a, ntiles_of(n), (cudaStream_t)stream);
 }
 
 int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, double eb, float* y,
@@ -161,7 +227,11 @@ int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, 
   a.tw = 2.0 * eb;
   a.y = y;
   a.st = reinterpret_cast<Status*>(d_status);
-  k_tile_decode<<<(unsigned)ntiles_of(n), TB, SMEM_BYTES, (cudaStream_t)stream>>>(a);
+  static int cap = -1;
+  grid_cap(k_tile_decode, DEC_SMEM_BYTES, cap);
+  const uint64_t want = (ntiles_of(n) + WARPS - 1) / WARPS;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
+  k_tile_decode<<<grid, CTA_THREADS, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -171,7 +241,7 @@ uint64_t gz_index_workspace_bytes(uint64_t payload_len) {
   // exit + count tables, composed tables, chunk entries, g32 (sized by the
   // largest possible block count: 5 bytes per block)
   const uint64_t nb_max = payload_len / 5 + 2;
-  return 64 + nseg * NE * 4 + nch * NE * 8 + nch * 16 + ((nb_max + 31) / 32) * 8 + 256;
+  return 64 + nseg * NE * 4 + nch * NE * 8 + nch * 16 + ((nb_max + GROUP - 1) / GROUP) * 8 + 256;
 }
 
 int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sidecar, void* ws, uint64_t ws_bytes,
@@ -202,7 +272,7 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   iw.cbase = reinterpret_cast<unsigned long long*>(take(nch * 8));
   // a block has at least 5 bytes: more blocks than that cannot be walked
   const uint64_t nb_eff = std::min<uint64_t>(nblocks(n), payload_len / 5 + 2);
-  iw.g32 = reinterpret_cast<unsigned long long*>(take(((nb_eff + 31) / 32) * 8));
+  iw.g8 = reinterpret_cast<unsigned long long*>(take(((nb_eff + GROUP - 1) / GROUP) * 8));
   const uint8_t* payload = blob + HEADER_BYTES;
   idx_segments<<<(unsigned)nseg, 160, 0, s>>>(payload, payload_len, iw);
   const size_t csm = (size_t)CH * NE * 4;
@@ -234,11 +304,13 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView so = sidecar_view(sidecar_out, m);
-  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0};
+  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0};
   a.nseg = 1;
-  a.nctas = nctas_of(m);
   a.qp = make_qparams(eb);
-  a.ws = reinterpret_cast<TileWs*>(ws);
+  const WsView wv = carve(ws, ntiles_of(m));
+  a.ws = wv.hdr;
+  a.tile_rel = wv.tile_rel;
+  a.scratch = wv.scratch;
   a.st = reinterpret_cast<Status*>(d_status);
   SidecarView si = sidecar_view(sidecar_in, m);
   a.in_blob = blob_in;
@@ -247,7 +319,13 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   a.in_tw = 2.0 * eb;
   a.op = op;
   a.acc_out = acc_out;
-  return launch_encode<SRC_STEP, 1>(a, (cudaStream_t)stream);
+  return launch_encode<SRC_STEP, 1>(a, ntiles_of(m), (cudaStream_t)stream);
+}
+
+uint64_t gz_segments_workspace_bytes(const uint64_t* h_counts, uint32_t nseg) {
+  uint64_t tiles = 0;
+  for (uint32_t i = 0; i < nseg; ++i) tiles += ntiles_of(h_counts[i]);
+  return ws_bytes_for_tiles(tiles);
 }
 
 int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,
@@ -256,37 +334,40 @@ int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg
                          gz_stream_t stream) {
   if (!check_eb(eb)) return GZ_EBOUND;
   if (!h_counts || !payload || !h_seg_blob_off || !d_seg_len || !ws || !d_status) return GZ_EINVAL;
-  uint64_t total = 0, nctas_all = 0;
+  uint64_t total = 0, tiles_all = 0;
   for (uint32_t i = 0; i < nseg; ++i) {
     total += h_counts[i];
-    nctas_all += nctas_of(h_counts[i]);
+    tiles_all += ntiles_of(h_counts[i]);
     if (!aligned16(payload + h_seg_blob_off[i])) return GZ_EINVAL;
   }
   if (total && !x) return GZ_EINVAL;
-  if (ws_bytes < 32 + 8 * (nctas_all + 1)) return GZ_EINVAL;
+  if (ws_bytes < ws_bytes_for_tiles(tiles_all)) return GZ_EINVAL;
   const QParams qp = make_qparams(eb);
-  uint64_t xoff = 0;
+  const WsView wv = carve(ws, tiles_all);
+  uint64_t xoff = 0, tile_base = 0;
   for (uint32_t s0 = 0; s0 < nseg; s0 += MAXSEG) {
     EncodeArgs<MAXSEG> a;
     std::memset(&a, 0, sizeof(a));
     const uint32_t cnt = std::min<uint32_t>(MAXSEG, nseg - s0);
-    uint64_t base = 0;
+    uint64_t tiles = 0;
     for (uint32_t j = 0; j < cnt; ++j) {
       const uint32_t i = s0 + j;
       const uint64_t n = h_counts[i];
       SidecarView sv{nullptr, nullptr};
       if (sidecars) sv = sidecar_view(reinterpret_cast<uint8_t*>(sidecars) + h_seg_sidecar_off[i], n);
-      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, base};
-      base += nctas_of(n);
+      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, tiles};
+      tiles += ntiles_of(n);
       xoff += n;
     }
     a.nseg = (int)cnt;
-    a.nctas = base;
     a.qp = qp;
-    a.ws = reinterpret_cast<TileWs*>(ws);
+    a.ws = wv.hdr;
+    a.tile_rel = wv.tile_rel + tile_base;
+    a.scratch = wv.scratch + tile_base * (uint64_t)TILE_SLOT;
     a.st = reinterpret_cast<Status*>(d_status);
-    const int rc = launch_encode<SRC_PLAIN, MAXSEG>(a, (cudaStream_t)stream);
+    const int rc = launch_encode<SRC_PLAIN, MAXSEG>(a, tiles, (cudaStream_t)stream);
     if (rc) return rc;
+    tile_base += tiles;
   }
   return 0;
 }

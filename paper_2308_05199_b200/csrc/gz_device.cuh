@@ -5,38 +5,42 @@
 //   block: width byte w (0..32, 255 = raw), the first value verbatim (f32 LE),
 //   then 31 zigzag codes packed LSB-first at w bits (raw: all values verbatim).
 //
-// Device layout ("tile" = GZ_TB consecutive 32-value blocks = one CTA):
-//   * one thread per 32-value block runs the closed-loop quantizer
-//     (codec.py:188-216) serially over its 31 steps;
-//   * input tiles are staged in shared memory with a 128B XOR swizzle so that
-//     both the coalesced fill and the per-thread row reads are conflict-free;
-//   * compressed bytes are packed into a shared-memory staging area, block
-//     offsets come from a CTA scan + a decoupled look-back across tiles
-//     (codec.py:241-243 np.cumsum), and the tile is written out with aligned
-//     16-byte stores (which may target a peer GPU's memory over NVLink);
-//   * a sidecar (u64 byte offset per tile + u16 offset per 32-block group)
-//     lets decoders find block starts without the sequential walk of
-//     codec.py:305-320.  The blob itself stays bit-exact.
+// Device layout: the unit of work is a WARP TILE = 32 consecutive 32-value
+// blocks (4 KB of input), one block per lane.  Each warp of a persistent grid
+// loops over warp tiles in ticket order with no CTA-wide barrier:
+//   * the next tile's values stream into the warp's second shared-memory
+//     buffer (cp.async) while the current one is quantised; tiles are stored
+//     with a 128B XOR swizzle so that both the coalesced fill and the
+//     per-lane row reads are free of bank conflicts;
+//   * every lane runs the closed-loop quantizer (codec.py:188-216) serially
+//     over the 31 steps of its block;
+//   * block sizes are scanned with warp shuffles, tile offsets come from a
+//     warp-wide decoupled look-back across tiles (codec.py:241-243 np.cumsum),
+//     and the packed tile is written with aligned 16-byte stores (which may
+//     target a peer GPU's memory over NVLink);
+//   * a sidecar (u64 payload offset per tile + u16 offset of every 8th block
+//     inside its tile) lets decoders find block starts with 8-step walks
+//     instead of the sequential walk of codec.py:305-320.  The blob itself
+//     stays bit-exact.
 //
 // Numerics: compile with --fmad=false.  Every f64 operation mirrors one numpy
-// ufunc of the reference; see closed_loop_step() for the exactness argument
+// ufunc of the reference; see fast_block() for the exactness argument
 // behind the f32 fast path.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
-
-#ifndef GZ_TB
-#define GZ_TB 128
-#endif
 
 namespace gz {
 
 constexpr int BLOCK = 32;           // codec.py:42
 constexpr int HEADER_BYTES = 24;    // codec.py:43-44
 constexpr int RAW_WIDTH = 255;      // codec.py:45
-constexpr int TB = GZ_TB;           // blocks per tile == threads per CTA
-constexpr int GROUPS = TB / 32;     // 32-block groups per tile (sub-offsets)
-constexpr int TILE_VALUES = TB * BLOCK;
+constexpr int TB = 32;              // blocks per warp tile (one per lane)
+constexpr int GROUP = 8;            // blocks per sidecar sub-offset
+constexpr int GROUPS = TB / GROUP;  // sub-offsets per tile
+constexpr int WARPS = 4;            // independent warps per CTA
+constexpr int CTA_THREADS = 32 * WARPS;
+constexpr int TILE_VALUES = TB * BLOCK;                    // 1024 values, 4 KB
 constexpr int MAX_BLOCK_BYTES = 1 + 4 * BLOCK;             // raw block, 129
 constexpr int STAGE_BYTES = TB * MAX_BLOCK_BYTES + 64;     // packed tile + slack
 constexpr int STAGE_WORDS = STAGE_BYTES / 4;
@@ -44,20 +48,23 @@ constexpr float MAGIC32 = 12582912.0f;                     // 1.5 * 2^23
 constexpr int MAGIC32_BITS = 0x4B400000;
 
 // ---- device workspace: zero-initialised once, reused by every launch -------
-// status[t] = gen(16) | flag(2) | value(46).  flag 1 = tile aggregate,
-// flag 2 = inclusive prefix.  `gen` advances when the last CTA of a launch
-// finishes, so no per-launch memset is needed and CUDA-graph replay is safe.
+// Layout: this header, status[MAXGRID], tile_rel[ntiles] (u32), scratch.
+// status[c] = gen(16) | flag(2) | value(46): flag 1 = CTA aggregate.  `gen`
+// advances when the last CTA of a launch retires, so no per-launch memset is
+// needed and CUDA-graph replay is safe.
+constexpr int MAXGRID = 4096;
+constexpr int TILE_SLOT = 4160;  // scratch bytes reserved per tile (>= 32 * 129, 16-aligned)
 struct TileWs {
   unsigned long long ticket;
   unsigned long long done;
   unsigned long long gen;
   unsigned long long pad;
-  unsigned long long status[1];  // [ntiles]
+  unsigned long long status[MAXGRID];
 };
 
 struct Status {                          // error reporting (host-reset to ~0)
   unsigned long long first_nonfinite;    // codec.py:83-85
-  unsigned long long decode_error;       // (block << 8) | code, min over blocks
+  unsigned long long decode_error;       // (block << 24) | (width << 8) | code, min over blocks
   unsigned long long pad[2];
 };
 enum DecodeErr : unsigned { DE_WIDTH = 1, DE_TRUNC = 2, DE_TRAIL = 3, DE_SIDECAR = 4, DE_HEADER = 5 };
@@ -65,16 +72,17 @@ enum DecodeErr : unsigned { DE_WIDTH = 1, DE_TRUNC = 2, DE_TRAIL = 3, DE_SIDECAR
 struct QParams {
   double tw;     // fl64(2*eb), codec.py:188
   double eb;
-  float rtw;     // RN32(1/tw)            (fast path only)
-  float kx;      // >= 2^-23 / tw         (fast path only)
-  float thr;     // 0.5 - margin          (fast path only)
+  float rtw;     // RN32(1/tw)                       (fast path only)
+  float thr;     // 0.5 - 2^-20: rounding margin      (fast path only)
+  float elo;     // <= eb * (1 - 2^-22), binary32     (fast path only)
+  float ehi;     // >= eb * (1 + 2^-22), binary32     (fast path only)
   int fast;      // 1 if tw lies in the range where the fast path is proven exact
 };
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 // ---------------------------------------------------------------------------
-// shared-memory tile of TB rows x 32 floats, 128-byte rows, 16-byte chunks
+// shared-memory warp tile of 32 rows x 32 floats, 128-byte rows, 16-byte chunks
 // XOR-swizzled by (row & 7): coalesced fills and per-row float4 reads are
 // both free of bank conflicts.
 __device__ __forceinline__ int xs_index(int row, int chunk) { return row * 32 + ((chunk ^ (row & 7)) << 2); }
@@ -119,49 +127,77 @@ __device__ __noinline__ StepOut slow_step(float prev32, float x, double tw, doub
   return o;
 }
 
-// One step of the closed loop.  prev32/prev64 hold the previous reconstructed
-// value (f32 and its exact f64).  Returns the zigzag code (codec.py:131-139).
-//
-// Fast path (f32 pipe, no conversions on the quantisation side):
-//   vf = RN32(RN32(x - prev) * RN32(1/tw)) approximates v = fl64(fl64(x-prev)/tw)
-//   with |vf - v| <= 3.01 * 2^-24 |v| (+ 2^-149 when subnormal).
-//   m = vf + 1.5*2^23 gives RNE(vf) exactly for |vf| < 2^21, fr = vf - RNE(vf).
-//   If  |fr| + 2^-21 |vf| + kx |x| < thr  (thr = 0.5 - 2^-20 - 2^-23) then
-//     * |v| is at distance > 2^-21 from every half-integer, so the reference's
-//       floor(fl64(|v| + 0.5)) * sign(v) equals RNE(vf) (ties impossible);
-//     * |q| < 2^21: no overflow;
-//     * the reconstruction error |rec - x| <= eb is guaranteed: it is bounded by
-//       tw (|fr| + 2^-22.4 |vf|) + ulp32(t)/2 + 2^-53(|t| + |q tw|), and
-//       kx |x| >= 2^-23 |x| / tw covers the rounding terms.
-//   The reconstruction itself (codec.py:205-207) is always computed in binary64
-//   exactly as the reference does: rec = RN32(fl64(prev + fl64(q * tw))).
-// Otherwise slow_step() replays the reference arithmetic verbatim.
-__device__ __forceinline__ uint32_t closed_loop_step(float x, float& prev32, double& prev64, const QParams& P,
-                                                      int& flags) {
-  int q;
-  bool ok = false;
-  float m = 0.f;
-  if (P.fast) {
-    float d32 = __fsub_rn(x, prev32);
-    float vf = __fmul_rn(d32, P.rtw);
-    m = __fadd_rn(vf, MAGIC32);
-    float qf = __fsub_rn(m, MAGIC32);
-    float fr = __fsub_rn(vf, qf);
-    float c = fmaf(fabsf(x), P.kx, fmaf(fabsf(vf), 0x1p-21f, fabsf(fr)));
-    ok = c < P.thr;
-  }
-  if (ok) {
-    q = __float_as_int(m) - MAGIC32_BITS;
-    double t = __dadd_rn(prev64, __dmul_rn(i32_to_f64(q), P.tw));
-    prev32 = __double2float_rn(t);
-  } else {
-    StepOut o = slow_step(prev32, x, P.tw, P.eb);
-    q = o.code;
+// Exact replay of one block with the reference arithmetic (codec.py:188-219),
+// writing the zigzag codes (codec.py:131-139) to z[0..cnt-2].  Used for the
+// partial final block, for blocks the fast pass could not prove, and for all
+// blocks when eb lies outside the fast path's range.  Returns the zigzag OR
+// and ORs overflow / error / non-finite flags into *flags.
+__device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, double tw, double eb, uint32_t* z,
+                                            int* flags) {
+  float prev32 = xs_row_vals[0];
+  int f = isfinite(prev32) ? 0 : 4;
+  uint32_t zor = 0;
+  for (int j = 1; j < cnt; ++j) {
+    const StepOut o = slow_step(prev32, xs_row_vals[j], tw, eb);
     prev32 = o.rec;
-    flags |= o.flags;
+    f |= o.flags;
+    const uint32_t zz = ((uint32_t)o.code << 1) ^ (uint32_t)(o.code >> 31);
+    z[j - 1] = zz;
+    zor |= zz;
   }
-  prev64 = (double)prev32;
-  return ((uint32_t)q << 1) ^ (uint32_t)(q >> 31);
+  for (int j = cnt; j < 32; ++j) z[j - 1 < 0 ? 0 : j - 1] = 0;
+  *flags |= f;
+  return zor;
+}
+
+// Branch-free fast pass over one full 32-value block (f32 pipe for the
+// quantisation decision, binary64 for the reconstruction).
+// Returns FB_PACKED (codes exact, every |rec - x| <= eb), FB_RAW (codes
+// exact and some |rec - x| > eb: the block is stored raw, codec.py:238) or
+// FB_SLOW (a step could not be proven; replay with slow_block()).
+//
+// Per step, with prev = previous reconstruction (f32 prev32, exact f64 prev64):
+//   vf = RN32(RN32(x - prev) * RN32(1/tw)) approximates the reference's
+//   v = fl64(fl64(x-prev)/tw) with |vf - v| <= 3.01 * 2^-24 |v|.
+//   m = vf + 1.5*2^23 holds RNE(vf) for |vf| < 2^21; fr = vf - RNE(vf).
+//   If |fr| + 2^-21 |vf| < 0.5 - 2^-20 then |v| is more than 2^-21 away from
+//   every half-integer, so floor(fl64(|v|+0.5))*sign(v) == RNE(vf), and
+//   |q| < 2^21 (no overflow, codec.py:201-204).
+//   The reconstruction rec = RN32(fl64(prev + fl64(q*tw))) is computed exactly
+//   as codec.py:205-207 does.  The error test of codec.py:208-210 is decided
+//   in binary32: e = RN32(|rec - x|) has relative error <= 2^-24, so
+//   e < elo (<= eb (1 - 2^-22)) proves |rec - x| <= eb and e > ehi
+//   (>= eb (1 + 2^-22)) proves |rec - x| > eb; only e in [elo, ehi] is undecided.
+enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
+
+__device__ __forceinline__ int fast_block(const float* xs, int row, double tw, float rtw, float thr, float elo,
+                                          float ehi, uint32_t (&z)[31], float& x0) {
+  float4 c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, 0));
+  float prev32 = c4.x;
+  x0 = c4.x;
+  double prev64 = (double)prev32;
+  bool rnd = true, ge = false, gt = false;
+#pragma unroll
+  for (int j = 1; j < 32; ++j) {
+    if ((j & 3) == 0) c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, j >> 2));
+    const float x = (j & 3) == 0 ? c4.x : (j & 3) == 1 ? c4.y : (j & 3) == 2 ? c4.z : c4.w;
+    const float vf = __fmul_rn(__fsub_rn(x, prev32), rtw);
+    const float m = __fadd_rn(vf, MAGIC32);
+    const float fr = __fsub_rn(vf, __fsub_rn(m, MAGIC32));
+    rnd &= fmaf(fabsf(vf), 0x1p-21f, fabsf(fr)) < thr;
+    const uint32_t qb = (uint32_t)__float_as_int(m) + 0x34C00000u;  // q ^ 0x80000000
+    const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)qb), 4503601774854144.0);
+    const double t = __dadd_rn(prev64, __dmul_rn(qd, tw));
+    prev32 = __double2float_rn(t);
+    prev64 = (double)prev32;
+    const float e = fabsf(__fsub_rn(prev32, x));
+    ge |= e >= elo;
+    gt |= e > ehi;
+    z[j - 1] = ~((qb << 1) ^ (uint32_t)((int)qb >> 31));            // zigzag(q)
+  }
+  if (!rnd) return FB_SLOW;
+  if (gt) return FB_RAW;
+  return ge ? FB_SLOW : FB_PACKED;
 }
 
 // ---------------------------------------------------------------------------

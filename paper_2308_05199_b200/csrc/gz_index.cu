@@ -14,7 +14,7 @@
 //   K4 idx_emit     : per chunk, derive each segment's actual entry, re-walk
 //                     the true chain with true block indices, apply the
 //                     reference's checks in walk order (first failing block
-//                     wins), and record the start of every 32nd block.
+//                     wins), and record the start of every 8th block.
 //   K5 idx_sidecar  : convert those starts into the sidecar layout.
 #include "gz_device.cuh"
 
@@ -33,7 +33,7 @@ struct IndexWs {
   unsigned* ccount;       // [nchunk][NE]
   long long* centry;      // [nchunk] actual entry (offset in first segment), <0 if unreachable
   unsigned long long* cbase;  // [nchunk] block index of the first start in the chunk
-  unsigned long long* g32;    // [ceil(nb/32)] payload offset of block 32k
+  unsigned long long* g8;     // [ceil(nb/8)] payload offset of block 8k
 };
 
 __device__ __forceinline__ int full_size(int w) { return w == RAW_WIDTH ? 1 + 4 * BLOCK : 5 + (31 * w + 7) / 8; }
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
       idx_error(st, blk, w, DE_WIDTH);
       return;
     }
-    if ((blk & 31) == 0) ws.g32[blk >> 5] = pos;
+    if ((blk & (GROUP - 1)) == 0) ws.g8[blk / GROUP] = pos;
     pos += size;
     if (pos > psize) {  // 319-320
       idx_error(st, blk, 0, DE_TRUNC);
@@ -180,13 +180,15 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
 __global__ void idx_sidecar(const IndexWs ws, uint64_t n, uint64_t psize, uint64_t* tile_off, uint16_t* sub_off) {
   const uint64_t nb = (n + BLOCK - 1) / BLOCK;
   const uint64_t ntiles = (nb + TB - 1) / TB;
-  const uint64_t ng = (nb + 31) / 32;
+  const uint64_t ng = (nb + GROUP - 1) / GROUP;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i < ntiles) tile_off[i] = ws.g32[i * GROUPS];
+  if (i < ntiles) tile_off[i] = ws.g8[i * GROUPS];
   if (i == ntiles) tile_off[ntiles] = psize;
   if (i < ntiles * GROUPS) {
     const uint64_t t = i / GROUPS;
-    sub_off[i] = (uint16_t)(i < ng ? ws.g32[i] - ws.g32[t * GROUPS] : 0);
+    // groups past the last block point at the end of the tile
+    const uint64_t tend = (t + 1 < ntiles) ? ws.g8[(t + 1) * GROUPS] : psize;
+    sub_off[i] = (uint16_t)((i < ng ? ws.g8[i] : tend) - ws.g8[t * GROUPS]);
   }
 }
 

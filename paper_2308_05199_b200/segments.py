@@ -23,12 +23,6 @@ def _align16(v: int) -> int:
     return (v + 15) & ~15
 
 
-def _nctas(c: int) -> int:
-    nb = -(-c // BLOCK)
-    tb = int(L.lib().gz_tile_blocks())
-    return max(-(-nb // tb), 1)
-
-
 @dataclass
 class SegmentBlobs:
     payload: torch.Tensor        # uint8, slot i at slot_off[i]
@@ -81,10 +75,9 @@ def compress_segments(x: torch.Tensor, counts, eb: float, ws: Workspace, stream=
     payload = torch.empty(max(pos, 16), dtype=torch.uint8, device=dev)
     sidecars = torch.empty(max(sc, 16), dtype=torch.uint8, device=dev)
     d_lens = torch.empty(max(nseg, 1), dtype=torch.int64, device=dev)
-    nctas = sum(_nctas(c) for c in counts)
-    tws = ws.tile_ws(32 + 8 * (nctas + 1))
     arr = ctypes.c_uint64 * max(nseg, 1)
     h_counts, h_slot, h_sc = arr(*counts), arr(*slot_off), arr(*sc_off)
+    tws = ws.tile_ws(int(lib.gz_segments_workspace_bytes(h_counts, nseg)))
     if check:
         ws.reset_status(stream)
     L.check(lib.gz_compress_segments(x.data_ptr(), h_counts, nseg, float(eb), payload.data_ptr(), h_slot,
