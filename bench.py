@@ -1,0 +1,390 @@
+"""Benchmark driver (one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workloads (BASELINE.json metric "gZ-Allreduce effective GB/s at 1-8 B200 vs
+NCCL; compressor HBM GB/s"):
+
+* N = 1  -> configs[0]: compress/decompress round trip of the synthetic smooth
+  float32 field (2^24 values, eb = 1e-4, block 32).  value = codec HBM GB/s =
+  algorithmic bytes (4n + |blob| per compress, |blob| + 4n per decompress) /
+  device time.  L2 (126 MB) is flushed before every timed step.
+* N > 1  -> configs[1]: compressed ring Allreduce (compressed reduce-scatter +
+  compress-once allgather) of a 512 MiB float32 field per rank, eb = 1e-4,
+  one process per GPU over NVLink peer memory; value = effective GB/s =
+  uncompressed bytes per rank / max-over-ranks device time (NCCL's algbw),
+  with NCCL all_reduce on the same tensors measured alongside.
+
+--impl reference times the reference algorithm on the host CPU (the C
+restatement in oracle/, all host threads) on the same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gZ-Allreduce effective GB/s at 1-8 B200 vs NCCL; compressor HBM GB/s"
+EB = 1e-4
+N_CFG1 = 1 << 24
+S_CFG2 = 512 << 20  # bytes per rank
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                self.samples.append([v.strip() for v in out.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        import statistics
+
+        sm = [float(s[0]) for s in self.samples if s and s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if len(s) > 1 and s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 2 + i and s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (C restatement of the reference codec, all host threads)
+# ---------------------------------------------------------------------------
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_codec_gbs(x, eb: float, threads: int, max_seconds: float = 20.0, steps: int = 1):
+    """Round-trip codec throughput of the CPU oracle on a bounded sample."""
+    from oracle import oracle as O
+
+    t_best = None
+    blob = None
+    done = 0
+    t_start = time.perf_counter()
+    while done < steps and (time.perf_counter() - t_start) < max_seconds:
+        t0 = time.perf_counter()
+        blob = O.compress(x, eb, threads=threads)
+        O.decompress(blob, threads=threads)
+        dt = time.perf_counter() - t0
+        t_best = dt if t_best is None else min(t_best, dt)
+        done += 1
+    nbytes = 2 * (4 * x.size + len(blob))
+    return nbytes / t_best / 1e9, t_best, len(blob), done
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host CPU."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+
+    threads = cpu_threads()
+    if args.gpus <= 1:
+        x = O.smooth_field(N_CFG1)
+        cpu_codec_gbs(x, EB, threads, steps=max(1, min(args.warmup, 1)))  # warm
+        gbs, t, L, done = cpu_codec_gbs(x, EB, threads, steps=args.steps, max_seconds=60.0)
+        line = {"metric": METRIC, "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus, "steps": done,
+                "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32->u8 (f64 closed loop)", "data": "synthetic smooth field",
+                "impl": "reference",
+                "config": {"workload": "cfg1 compress/decompress round trip, 2^24 f32, eb=1e-4, block=32"},
+                "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "port",
+                                 "sample": "full cfg1 field (2^24 f32), best of steps"},
+                "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    else:
+        # ring allreduce on the CPU for N ranks over a bounded per-rank sample
+        N = args.gpus
+        n = 1 << 21  # 8 MiB per rank
+        bufs = [O.smooth_field(n, 0.37 * r) for r in range(N)]
+        t0 = time.perf_counter()
+        O.ring_allreduce(bufs, EB)
+        dt = time.perf_counter() - t0
+        gbs = 4 * n / dt / 1e9
+        line = {"metric": METRIC, "value": round(gbs, 5), "unit": "GB/s", "n_gpus": N, "steps": 1,
+                "warmup": 0, "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32->u8 (f64 closed loop)", "data": "synthetic smooth field",
+                "impl": "reference",
+                "config": {"workload": f"ring-allreduce eb=1e-4, N={N} virtual ranks on the host, 8 MiB per rank sample"},
+                "cpu_baseline": {"value": round(gbs, 5), "unit": "GB/s", "cores": 1, "kind": "port",
+                                 "sample": "8 MiB per rank (bounded sample of the 512 MiB workload)"},
+                "e2e": {"value": round(gbs, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm, N = 1: codec round trip
+# ---------------------------------------------------------------------------
+
+
+def bench_codec(args):
+    import numpy as np
+    import torch
+
+    import paper_2308_05199_b200 as gz
+    from paper_2308_05199_b200 import _lib as L
+    from oracle import oracle as O
+
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    lib = L.lib()
+    n = N_CFG1
+    xh = O.smooth_field(n)
+    x = torch.from_numpy(xh).to(dev)
+    ws = gz.Workspace(dev)
+    blob0 = gz.compress(x, EB, ws)
+    Lb = len(blob0)
+    # persistent buffers for the timed loop (the public API allocates per call)
+    cap = int(lib.gz_compress_bound(n))
+    out = torch.empty(cap, dtype=torch.uint8, device=dev)
+    sc = torch.empty(int(lib.gz_sidecar_bytes(n)), dtype=torch.uint8, device=dev)
+    tws = ws.tile_ws(int(lib.gz_workspace_bytes(n)))
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    s = stream.cuda_stream
+
+    def comp():
+        L.check(lib.gz_compress(x.data_ptr(), n, EB, 32, out.data_ptr(), cap, ws.len_ptr(), sc.data_ptr(), None,
+                                tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_compress")
+
+    def dec():
+        L.check(lib.gz_decompress_sidecar(out.data_ptr(), sc.data_ptr(), n, EB, y.data_ptr(), ws.status_ptr(), s),
+                "gz_decompress_sidecar")
+
+    for _ in range(max(args.warmup, 3)):
+        flush.zero_()
+        comp()
+        dec()
+    torch.cuda.synchronize()
+    tc, td = [], []
+    with ClockSampler(0) as clk:
+        torch.cuda.synchronize()
+        for _ in range(args.steps):
+            flush.zero_()  # L2 flush: 256 MB > 126 MB L2, outside the timed events
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            comp()
+            e1.record(stream)
+            dec()
+            e2.record(stream)
+            torch.cuda.synchronize()
+            tc.append(e0.elapsed_time(e1) * 1e-3)
+            td.append(e1.elapsed_time(e2) * 1e-3)
+    torch.cuda.synchronize()
+    # parity of the timed output against the oracle-pinned first blob
+    assert bytes(out[:Lb].cpu().numpy().tobytes()) == bytes(blob0), "timed blob differs"
+    t_c, t_d = sum(tc) / len(tc), sum(td) / len(td)
+    bytes_c = 4 * n + Lb
+    bytes_d = Lb + 4 * n
+    value = (bytes_c + bytes_d) / (t_c + t_d) / 1e9
+    peak, peak_kind = peaks()
+    achieved_c = bytes_c / t_c / 1e9
+
+    # e2e through the public API with host buffers: inputs in pinned host
+    # memory; each step = H2D + compress + D2H of the blob, then H2D of the
+    # blob + device indexing (reference blob, no sidecar) + decode + D2H
+    xp = torch.from_numpy(xh).pin_memory()
+    e2e_t = []
+    for i in range(max(3, min(args.steps, 10)) + 2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b = gz.compress(xp, EB, ws)
+        yb = gz.decompress(b, ws)
+        torch.cuda.synchronize()
+        if i >= 2:
+            e2e_t.append(time.perf_counter() - t0)
+    e2e = (bytes_c + bytes_d) / (sum(e2e_t) / len(e2e_t)) / 1e9
+    assert yb.numel() == n and bytes(b.numpy().tobytes()) == bytes(blob0)
+
+    # CPU baseline (oracle port, all host threads) on the same workload
+    thr = cpu_threads()
+    cpu_gbs, cpu_t, _, cpu_steps = cpu_codec_gbs(xh, EB, thr, max_seconds=15.0, steps=2)
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as f:
+                traffic = json.load(f).get("k_tile_encode_cfg1")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": round((t_c + t_d) * 1e3, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32->u8 (f64 closed loop)",
+        "data": "synthetic smooth field 0.5 sin(2pi i/65536) + 0.25 sin(2pi i/4099)",
+        "config": {"workload": "cfg1 compress/decompress round trip, 2^24 f32, eb=1e-4, block=32",
+                   "compressed_bytes": Lb, "compression_ratio": round(4 * n / Lb, 4),
+                   "l2": "flushed (256 MB write) before every timed step",
+                   "compress_us": round(t_c * 1e6, 2), "decompress_us": round(t_d * 1e6, 2),
+                   "compress_hbm_gbs": round(achieved_c, 1), "decompress_hbm_gbs": round(bytes_d / t_d / 1e9, 1)},
+        "roofline": {"bound": "hbm", "kernel": "k_tile_encode (compress)", "achieved": round(achieved_c, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved_c / peak, 4),
+                     "traffic": traffic, "algorithmic_bytes_per_launch": bytes_c},
+        "cpu_baseline": {"value": round(cpu_gbs, 4), "unit": "GB/s", "cores": thr, "kind": "port",
+                         "sample": f"full cfg1 field, best of {cpu_steps} round trips, C oracle with {thr} threads"},
+        "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n + Lb, "d2h_bytes_per_step": Lb + 4 * n,
+                "api": "compress(pinned host f32 tensor) -> pinned host blob; decompress(host blob) -> pinned host f32",
+                "wall_ms_per_step": round(sum(e2e_t) / len(e2e_t) * 1e3, 3)},
+        "gpu_launches": 2 * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# our arm, N > 1: compressed ring allreduce over NVLink peer memory
+# ---------------------------------------------------------------------------
+
+
+def bench_allreduce(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2308_05199_b200 import comm
+    from oracle import oracle as O
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    n = S_CFG1_elems = S_CFG2 // 4
+    xh = O.smooth_field(n, 0.37 * rank)
+    x = torch.from_numpy(xh).to(dev)
+    c = comm.Communicator(dist.group.WORLD, dev)
+    out = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        c.ring_allreduce(x, EB, out=out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    times = []
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            c.ring_allreduce(x, EB, out=out)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) * 1e-3)
+    t_local = sum(times) / len(times)
+    tt = torch.tensor([t_local], device=dev, dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    # NCCL comparator on the same tensor
+    y = x.clone()
+    for _ in range(3):
+        dist.all_reduce(y)
+    torch.cuda.synchronize()
+    dist.barrier()
+    nt = []
+    for _ in range(max(3, min(args.steps, 10))):
+        y.copy_(x)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        dist.all_reduce(y)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        nt.append(e0.elapsed_time(e1) * 1e-3)
+    tn = torch.tensor([sum(nt) / len(nt)], device=dev, dtype=torch.float64)
+    dist.all_reduce(tn, op=dist.ReduceOp.MAX)
+    nccl_gbs = S_CFG2 / float(tn.item()) / 1e9
+    value = S_CFG2 / t / 1e9
+    cr = c.compression_ratio()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": round(t * 1e3, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32 (compressed u8 wire, f64 closed loop)",
+            "data": "synthetic smooth field per rank (phase 0.37 r)",
+            "config": {"workload": "ring-allreduce (compressed RS + compress-once AG), 512 MiB f32 per rank, eb=1e-4",
+                       "parallelism": f"ring over {world} GPUs, NVLink peer memory",
+                       "nccl_allreduce_gbs": round(nccl_gbs, 2), "compression_ratio": cr,
+                       "l2": "inputs (512 MiB) larger than L2"},
+            "roofline": {"bound": "nvlink*CR", "achieved": round(value, 2), "peak": round(900.0 * (cr or 1.0), 1),
+                         "unit": "GB/s", "frac": round(value / (900.0 * (cr or 1.0)), 4), "traffic": None},
+            "e2e": None,
+            "gpu_launches": c.launches_per_call * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus <= 1 and world <= 1:
+        return bench_codec(args)
+    return bench_allreduce(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -154,6 +154,11 @@ def _as_device_f32(data, device=None) -> tuple[torch.Tensor, bool]:
         if data.dim() != 1:
             raise ValueError("expected a flat 1-D sequence of binary32 values")
         return data.detach().to(torch.float32).contiguous(), True
+    if isinstance(data, torch.Tensor):  # host tensor (ideally pinned): async H2D
+        if data.dim() != 1:
+            raise ValueError("expected a flat 1-D sequence of binary32 values")
+        dev = _device_of(device)
+        return data.detach().to(torch.float32).contiguous().to(dev, non_blocking=True), False
     x = np.ascontiguousarray(data, dtype="<f4")
     if x.ndim != 1:
         raise ValueError("expected a flat 1-D sequence of binary32 values")
@@ -166,7 +171,8 @@ def compress(data, eb, workspace: Workspace | None = None, *, block: int = BLOCK
     """Compress binary32 values under an absolute error bound (codec.py:149-270).
 
     Host input -> ``bytes`` (byte-identical to the reference).  CUDA tensor
-    input -> :class:`DeviceBlob`.  Rejects non-finite input (``ValueError``
+    input -> :class:`DeviceBlob`.  Host torch tensor (pinned) -> pinned host
+    uint8 tensor holding the reference bytes.  Rejects non-finite input (``ValueError``
     naming the first bad offset) and non-positive bounds.
     """
     _check_block(block)
@@ -192,6 +198,11 @@ def compress(data, eb, workspace: Workspace | None = None, *, block: int = BLOCK
     db = DeviceBlob(blob[:length], sidecar, n, ebf, offs[:nb] if offs is not None else None)
     if on_dev:
         return db
+    if isinstance(data, torch.Tensor):  # host tensor in -> pinned host uint8 tensor out
+        host = torch.empty(length, dtype=torch.uint8, pin_memory=True)
+        host.copy_(blob[:length], non_blocking=True)
+        (stream or torch.cuda.current_stream()).synchronize()
+        return host
     out = bytes(db)
     if return_offsets:
         return out, offs[:nb].cpu().numpy()
@@ -255,12 +266,31 @@ def decompress(blob, workspace: Workspace | None = None, *, stream=None, check: 
     """Decode a compressed blob back to float32 values (codec.py:284-369).
 
     ``bytes``-like input -> ``np.ndarray``; :class:`DeviceBlob` or CUDA uint8
-    tensor -> ``torch.Tensor`` on that device.  Raises :class:`DecodeError` on
+    tensor -> ``torch.Tensor`` on that device; host uint8 tensor -> pinned
+    host float32 tensor.  Raises :class:`DecodeError` on
     malformed headers, truncated payloads or unknown width codes.
     """
     if isinstance(blob, DeviceBlob):
         ws = _ws_for(workspace, blob.data.device)
         return _decode_with_sidecar(blob.data, blob.sidecar, blob.n, blob.eb, ws, stream, check)
+    if isinstance(blob, torch.Tensor) and not blob.is_cuda:  # host uint8 tensor (ideally pinned)
+        hb = blob.reshape(-1)
+        total = int(hb.numel())
+        n, eb = _parse_header(hb[:HEADER_BYTES].numpy().tobytes())
+        if n == 0:
+            if total > HEADER_BYTES:
+                raise DecodeError("trailing bytes after empty payload")
+            return torch.empty(0, dtype=torch.float32)
+        dev = _device_of(workspace.device if workspace is not None else None)
+        ws = _ws_for(workspace, dev)
+        buf = ws.get("decompress.blob", total + 64)
+        buf[:total].copy_(hb, non_blocking=True)
+        sidecar = index(buf, n, total - HEADER_BYTES, ws, stream)
+        y = _decode_with_sidecar(buf, sidecar, n, eb, ws, stream, check)
+        out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        out.copy_(y, non_blocking=True)
+        (stream or torch.cuda.current_stream()).synchronize()
+        return out
     on_dev = isinstance(blob, torch.Tensor) and blob.is_cuda
     if on_dev:
         head = bytes(blob[:HEADER_BYTES].cpu().numpy().tobytes())

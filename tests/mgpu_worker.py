@@ -1,0 +1,70 @@
+"""Multi-GPU parity worker (launched by tests/test_comm_gpu.py via torchrun).
+
+Each rank runs Communicator.ring_allreduce on its own GPU (NVLink peer memory)
+and compares its output byte-for-byte with the CPU oracle's per-rank output
+for the same inputs (and with the reference's golden per-rank outputs for the
+golden cases of matching rank count).
+"""
+
+import os
+import sys
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+
+def main():
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    from oracle import oracle as O
+    from paper_2308_05199_b200 import comm
+    import golden_data as G
+
+    c = comm.Communicator(dist.group.WORLD, dev)
+    failures = []
+    checked = 0
+    # golden cases (reference outputs) with this rank count
+    for case in G.ring_cases():
+        if case.algo != "ring-allreduce" or case.N != world:
+            continue
+        x = torch.from_numpy(np.ascontiguousarray(case.inputs[rank], np.float32)).to(dev)
+        for rep in range(2):  # twice: flags and slots are reused across calls
+            out = c.ring_allreduce(x, case.eb, case.op)
+            torch.cuda.synchronize()
+            if out.cpu().numpy().tobytes() != case.outputs[rank].tobytes():
+                failures.append(f"golden N={case.N} n={case.n} op={case.op} rep={rep}")
+            checked += 1
+    # larger seeded inputs vs the oracle
+    rng = np.random.default_rng(7)
+    for n, op, eb in ((1 << 20, "sum", 1e-4), (3_000_017, "sum", 1e-3), (777_777, "max", 1e-4), (1 << 22, "sum", 1e-5)):
+        bufs = [O.smooth_field(n, 0.37 * r) + np.random.default_rng(100 + r).normal(0, 1e-3, n).astype(np.float32)
+                for r in range(world)]
+        expect = O.ring_allreduce(bufs, eb, op)
+        x = torch.from_numpy(bufs[rank]).to(dev)
+        out = c.ring_allreduce(x, eb, op)
+        torch.cuda.synchronize()
+        if out.cpu().numpy().tobytes() != expect[rank].tobytes():
+            failures.append(f"oracle n={n} op={op} eb={eb}")
+        checked += 1
+    flag = torch.tensor([len(failures)], device=dev)
+    dist.all_reduce(flag)
+    if rank == 0:
+        print(f"mgpu ranks={world} checked={checked} failures={int(flag.item())}", flush=True)
+    if failures:
+        print(f"rank {rank} failures: {failures}", flush=True)
+    c.close()
+    dist.destroy_process_group()
+    sys.exit(1 if int(flag.item()) else 0)
+
+
+if __name__ == "__main__":
+    main()

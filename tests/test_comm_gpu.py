@@ -1,0 +1,34 @@
+"""Real multi-GPU ring allreduce (one process per GPU, NVLink peer memory)
+vs the reference / oracle per-rank outputs, bit-exact."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
+
+torch = pytest.importorskip("torch")
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+@pytest.mark.parametrize("nproc", sorted({2, min(NGPU, 4), min(NGPU, 8)} - {1}))
+def test_ring_allreduce_multi_gpu(nproc):
+    if nproc > NGPU:
+        pytest.skip("not enough GPUs")
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tests", "mgpu_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    sys.stdout.write(r.stdout[-4000:])
+    sys.stderr.write(r.stderr[-4000:])
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "failures=0" in r.stdout
