@@ -15,13 +15,11 @@ using namespace gz;
 
 namespace {
 
-constexpr size_t ENC_SMEM_BYTES = (size_t)WARPS * ENC_WARP_SMEM;  // per warp: two value tiles + staging
 constexpr size_t DEC_SMEM_BYTES = (size_t)WARPS * DEC_WARP_SMEM;  // per warp: value tile + two stagings
 constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-parameter budget)
 
 inline uint64_t nblocks(uint64_t n) { return (n + BLOCK - 1) / BLOCK; }
 inline uint64_t ntiles_of(uint64_t n) { return (nblocks(n) + TB - 1) / TB; }
-inline uint64_t nctas_of(uint64_t n) { return std::max<uint64_t>(ntiles_of(n), 1); }
 
 bool check_eb(double eb) { return std::isfinite(eb) && eb > 0.0; }
 
@@ -85,8 +83,10 @@ struct WsView {
   uint8_t* scratch;
 };
 inline uint64_t align16(uint64_t v) { return (v + 15) & ~15ull; }
+// header + per-tile sizes + scratch (per tile one slot; the warps' runs are
+// 128-byte aligned, hence up to 128 B of padding per warp)
 inline uint64_t ws_bytes_for_tiles(uint64_t tiles) {
-  return align16(sizeof(TileWs)) + align16(4 * tiles) + tiles * (uint64_t)TILE_SLOT + 64;
+  return align16(sizeof(TileWs)) + align16(4 * tiles) + 128 + tiles * (uint64_t)TILE_SLOT;
 }
 WsView carve(void* ws, uint64_t tiles) {
   uint8_t* p = reinterpret_cast<uint8_t*>(ws);
@@ -94,29 +94,38 @@ WsView carve(void* ws, uint64_t tiles) {
   v.hdr = reinterpret_cast<TileWs*>(p);
   v.tile_rel = reinterpret_cast<uint32_t*>(p + align16(sizeof(TileWs)));
   v.scratch = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(p + align16(sizeof(TileWs)) + align16(4 * tiles)) + 15) & ~(uintptr_t)15);
+      (reinterpret_cast<uintptr_t>(p + align16(sizeof(TileWs)) + align16(4 * tiles)) + 127) & ~(uintptr_t)127);
   return v;
 }
 
-// Grid = CTAs that fit at once (capped by the work); the CTAs are split over
-// segments in proportion to their tiles (at least one CTA per segment).
+// Grid = one CTA per SM (capped by the work); CTAs are split over segments in
+// proportion to their tiles (at least one CTA per segment).
 template <int SRC, int NSEG, bool FAST>
 int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
+  constexpr int NW = enc_warps(SRC);
+  const size_t smem = (size_t)NW * (SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4);
   static int cap = -1;
-  grid_cap(k_tile_encode<SRC, NSEG, FAST>, ENC_SMEM_BYTES, cap);
-  uint64_t G = std::min<uint64_t>((uint64_t)cap, (total_tiles + WARPS - 1) / WARPS);
+  if (cap < 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(k_tile_encode<SRC, NSEG, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_encode<SRC, NSEG, FAST>, 32 * NW, smem);
+    cap = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
+  }
+  uint64_t G = std::min<uint64_t>((uint64_t)cap, std::max<uint64_t>(1, (total_tiles + NW - 1) / NW));
   G = std::max<uint64_t>(G, (uint64_t)a.nseg);
-  uint64_t base = 0;
+  if (G > (uint64_t)MAXGRID) return GZ_EINVAL;
+  uint64_t base = 0, left = G - (uint64_t)a.nseg;
   for (int k = 0; k < a.nseg; ++k) {
     const uint64_t tk = ntiles_of(a.seg[k].n);
-    uint64_t ck = total_tiles ? (G * tk) / total_tiles : 1;
-    ck = std::max<uint64_t>(1, std::min<uint64_t>(ck, std::max<uint64_t>(1, (tk + WARPS - 1) / WARPS)));
+    const uint64_t extra = total_tiles ? (left * tk) / total_tiles : 0;
     a.seg[k].cta_base = base;
-    base += ck;
+    base += 1 + extra;
   }
-  if (base > (uint64_t)MAXGRID) return GZ_EINVAL;
   a.nctas = base;
-  k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, CTA_THREADS, ENC_SMEM_BYTES, s>>>(a);
+  a.total_tiles = total_tiles;
+  k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   return (int)cudaGetLastError();
 }
 
@@ -169,7 +178,15 @@ PFN_waitValue32 p_wait32() {
 
 }  // namespace
 
+// experiments only: per-warp timestamps of the next compress launch
+static unsigned long long* g_dbg = nullptr;
+
 extern "C" {
+
+int gz_debug_set_timestamps(void* p) {
+  g_dbg = reinterpret_cast<unsigned long long*>(p);
+  return 0;
+}
 
 uint64_t gz_compress_bound(uint64_t n) { return HEADER_BYTES + nblocks(n) * MAX_BLOCK_BYTES + 64; }
 uint64_t gz_num_tiles(uint64_t n) { return ntiles_of(n); }
@@ -205,6 +222,7 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   a.nseg = 1;
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
+  a.dbg = g_dbg;
   const WsView wv = carve(ws, ntiles_of(n));
   a.ws = wv.hdr;
   a.tile_rel = wv.tile_rel;

@@ -33,11 +33,13 @@ struct EncodeArgs {
   Seg seg[NSEG];
   int nseg;
   uint64_t nctas;          // CTAs (== grid), split over segments by cta_base
+  uint64_t total_tiles;    // tiles over all segments (phase A tickets)
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
   TileWs* ws;
-  uint32_t* tile_rel;      // per tile: offset inside its warp's scratch run
-  uint8_t* scratch;        // per tile TILE_SLOT bytes; a warp's tiles are packed back to back
+  unsigned long long* dbg; // optional per-warp timestamps (experiments)
+  uint32_t* tile_rel;      // per tile: compressed size (phase A -> phase B)
+  uint8_t* scratch;        // per tile one TILE_SLOT-byte slot (16-byte aligned)
   Status* st;
   // fused step only (NSEG == 1)
   const uint8_t* in_blob;  // received blob (header + payload)
@@ -59,6 +61,8 @@ struct DecodeArgs {
 };
 
 constexpr int ENC_WARP_SMEM = 2 * TILE_VALUES * 4 + STAGE_BYTES;  // two value tiles + staging
+// warps per encoder CTA (one CTA per SM): as many as shared memory allows
+__host__ __device__ constexpr int enc_warps(int src) { return src == 1 ? 16 : 24; }
 constexpr int DEC_WARP_SMEM = TILE_VALUES * 4 + 2 * STAGE_BYTES;  // value tile + two stagings
 
 // -------------------------------------------------------------------------
@@ -88,6 +92,12 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // Warp-synchronous fill of the swizzled tile xs[32][32] with src[v0, v0+nval):
 // asynchronous (cp.async) for a full 16-byte aligned tile, direct otherwise.
@@ -191,19 +201,10 @@ __device__ __forceinline__ void walk_groups(const uint32_t* stage, int base, int
   if (pos != gend) record_decode_error(st, b0 + g0 + gblk - 1, DE_SIDECAR);
 }
 
-// Decode this lane's block (walked by walk_groups) into its xs row.
-// MODE 0: xs = decoded.  MODE 1: xs = op(xs, decoded), collectives.py:32-39.
-template <int MODE>
-__device__ __forceinline__ void decode_row(const uint32_t* stage, int base, int nblk, uint64_t b0, uint64_t nb,
-                                           int last_cnt, double tw, float* xs, int op, const double* s_step,
-                                           const uint16_t* s_start, const uint8_t* s_w, int lane) {
-  const int row = lane;
-  if (row >= nblk || s_start[row] == 0xFFFF) return;
-  const int my_w = s_w[row];
-  const uint64_t gb = b0 + row;
-  const int cnt = (gb == nb - 1) ? last_cnt : 32;
-  const int p0 = base + s_start[row];
-  float out[32];
+// Values of one block (codec.py:331-369) from its staged bytes.
+__device__ __forceinline__ void decode_values(const uint32_t* stage, int base, int bstart, int my_w, int cnt, double tw,
+                                              const double* s_step, float* out) {
+  const int p0 = base + bstart;
   if (my_w == RAW_WIDTH) {  // codec.py:364-367
 #pragma unroll
     for (int j = 0; j < 32; ++j) out[j] = j < cnt ? __uint_as_float(lds_u32u(stage, p0 + 1 + 4 * j)) : 0.0f;
@@ -252,6 +253,20 @@ __device__ __forceinline__ void decode_row(const uint32_t* stage, int base, int 
       out[j] = j < cnt ? rec : 0.0f;
     }
   }
+}
+
+// Decode this lane's block (walked by walk_groups) into its xs row.
+// MODE 0: xs = decoded.  MODE 1: xs = op(xs, decoded), collectives.py:32-39.
+template <int MODE>
+__device__ __forceinline__ void decode_row(const uint32_t* stage, int base, int nblk, uint64_t b0, uint64_t nb,
+                                           int last_cnt, double tw, float* xs, int op, const double* s_step,
+                                           const uint16_t* s_start, const uint8_t* s_w, int lane) {
+  const int row = lane;
+  if (row >= nblk || s_start[row] == 0xFFFF) return;
+  const uint64_t gb = b0 + row;
+  const int cnt = (gb == nb - 1) ? last_cnt : 32;
+  float out[32];
+  decode_values(stage, base, s_start[row], s_w[row], cnt, tw, s_step, out);
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     float4* dst = reinterpret_cast<float4*>(xs + xs_index(row, c));
@@ -309,37 +324,40 @@ __device__ __forceinline__ void copy_to_unaligned(uint8_t* dst, const uint8_t* s
   }
 }
 
-// Append the staged tile (tile_bytes from smem) to the warp's scratch run at
-// byte offset `run` (16-byte aligned run start + arbitrary offset).
-__device__ __forceinline__ void stage_to_scratch(uint8_t* run_base, uint64_t run, const uint32_t* stage, int tile_bytes,
-                                                 int lane) {
-  if (!tile_bytes) return;
-  uint8_t* gdst = run_base + run;
-  const uintptr_t A = reinterpret_cast<uintptr_t>(gdst);
-  const uintptr_t E = A + (uintptr_t)tile_bytes;
-  const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cl = E & ~(uintptr_t)15;
-  const uint8_t* sb = reinterpret_cast<const uint8_t*>(stage);
-  if (cf < cl) {
-    const int off0 = (int)(cf - A);
-    const int sh = (off0 & 3) * 8;
-    const int nch = (int)((cl - cf) >> 4);
-    uint4* dst = reinterpret_cast<uint4*>(cf);
-    for (int c = lane; c < nch; c += 32) {
-      const int wi = (off0 >> 2) + 4 * c;
-      const uint32_t w0 = stage[wi], w1 = stage[wi + 1], w2 = stage[wi + 2], w3 = stage[wi + 3], w4 = stage[wi + 4];
-      uint4 v;
-      v.x = __funnelshift_r(w0, w1, sh);
-      v.y = __funnelshift_r(w1, w2, sh);
-      v.z = __funnelshift_r(w2, w3, sh);
-      v.w = __funnelshift_r(w3, w4, sh);
-      __stcg(dst + c, v);
+// One thread copies `len` bytes from a 16-byte aligned slot to an arbitrary
+// destination (possibly a peer GPU): byte stores up to the first 16-byte
+// boundary, aligned 16-byte stores (source re-aligned with funnel shifts),
+// byte stores for the tail.  Neighbouring tiles only share the edge chunks,
+// which are written byte-wise, so concurrent lanes never overlap.
+__device__ __forceinline__ void lane_copy(uint8_t* dst, const uint8_t* src, int len) {
+  if (len <= 0) return;
+  const int h = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+  for (int i = 0; i < h; ++i) dst[i] = src[i];
+  const int nch = (len - h) >> 4;
+  if (nch > 0) {
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + (h & ~15));
+    uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+    const int wo = (h >> 2) & 3, sh = (h & 3) * 8;
+    uint4 cur = __ldcg(s4);
+#pragma unroll 2
+    for (int c = 0; c < nch; ++c) {
+      const uint4 nxt = __ldcg(s4 + c + 1);
+      // words wo..wo+4 of the 8-word window (cur, nxt)
+      const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+      const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+      const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+      const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+      const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+      uint4 o;
+      o.x = __funnelshift_r(a0, a1, sh);
+      o.y = __funnelshift_r(a1, a2, sh);
+      o.z = __funnelshift_r(a2, a3, sh);
+      o.w = __funnelshift_r(a3, a4, sh);
+      d4[c] = o;
+      cur = nxt;
     }
-    const int head = (int)(cf - A), tail = (int)(E - cl);
-    if (lane < head) gdst[lane] = sb[lane];
-    if (lane >= 16 && lane - 16 < tail) gdst[tile_bytes - tail + (lane - 16)] = sb[tile_bytes - tail + (lane - 16)];
-  } else {
-    for (int i = lane; i < tile_bytes; i += 32) gdst[i] = sb[i];
   }
+  for (int i = h + 16 * nch; i < len; ++i) dst[i] = src[i];
 }
 
 struct SegGeom {
@@ -355,21 +373,111 @@ __device__ __forceinline__ SegGeom seg_geom(uint64_t n) {
   return g;
 }
 
-// Pass A for one warp tile (values in xs): quantise, pack into smem, append
-// to the warp's scratch run.  Returns the tile's compressed size.
+template <int NSEG>
+__device__ __forceinline__ int seg_of_tile(const EncodeArgs<NSEG>& a, uint64_t t) {
+  int k = 0;
+  if (NSEG > 1) {
+#pragma unroll 1
+    for (int i = 1; i < a.nseg; ++i)
+      if (a.seg[i].tile_base <= t) k = i;
+  }
+  return k;
+}
+
+// L2 policies: the input stream should not displace the scratch, which is
+// read back (and discarded) moments later.
+__device__ __forceinline__ uint64_t pol_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t pol_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void cp_async16_hint(void* sdst, const void* gsrc, uint64_t pol) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void discard_l2_line(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
+// Start loading tile `t` (global tile index) into xs (evict-first: the values
+// are read exactly once).
+template <int NSEG>
+__device__ __forceinline__ void prefetch_tile(const EncodeArgs<NSEG>& a, uint64_t t, float* xs, int lane, uint64_t pol) {
+  if (t < a.total_tiles) {
+    const Seg& S = a.seg[seg_of_tile(a, t)];
+    const uint64_t v0 = (t - S.tile_base) * TILE_VALUES;
+    const int nval = (int)umin64(S.n - v0, TILE_VALUES);
+    const float* p = S.x + v0;
+    if (nval == TILE_VALUES && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
+      const float4* p4 = reinterpret_cast<const float4*>(p);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int i = lane + 32 * j;
+        cp_async16_hint(xs + xs_index(i >> 3, i & 7), p4 + i, pol);
+      }
+    } else {
+      for (int i = lane; i < TILE_VALUES; i += 32) {
+        const float v = i < nval ? __ldcs(p + i) : 0.0f;
+        const int row = i >> 5, col = i & 31;
+        xs[xs_index(row, col >> 2) + (col & 3)] = v;
+      }
+    }
+  }
+  cp_async_commit();
+}
+
+// Values of this lane's block (the inputs of the quantiser), for the rare
+// paths that run after the codes have overwritten them in shared memory.
+template <int SRC, int NSEG>
+__device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg& S, uint64_t v0, int cnt,
+                                           const uint32_t* stage, int base, double tw, const double* s_step,
+                                           const uint16_t* s_start, const uint8_t* s_w, int lane, float* row) {
+  const float* src = S.x + v0 + (uint64_t)lane * 32;
+  for (int j = 0; j < 32; ++j) row[j] = j < cnt ? src[j] : 0.0f;
+  if (SRC == SRC_STEP) {
+    float dec[32];
+    decode_values(stage, base, s_start[lane], s_w[lane], cnt, tw, s_step, dec);
+    for (int j = 0; j < cnt; ++j) row[j] = a.op == OP_SUM ? __fadd_rn(row[j], dec[j]) : np_maximum(row[j], dec[j]);
+  }
+}
+
+// Phase A for one warp tile (values in xs): quantise and pack the tile into
+// `dst` starting at byte `pos0`.  In a run (carry mode) the tile continues the
+// previous tile's bytes: `carry` holds that tile's last partial word and the
+// function returns this tile's, instead of completing it with zeros.
 template <int SRC, int NSEG, bool FAST>
 __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
-                                           float* xs, uint32_t* stage, uint16_t* s_start, uint8_t* s_w,
-                                           const double* s_step, int lane) {
+                                           float* xs, uint32_t* dst, int pos0, bool run_mode, uint32_t& carry,
+                                           uint32_t* stage, uint16_t* s_start, uint8_t* s_w, const double* s_step,
+                                           uint64_t pol_keep, int lane) {
   const uint64_t nb = G.nb, b0 = tile * TB, v0 = b0 * BLOCK;
   const int last_cnt = G.last_cnt;
   const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
   const int nval = (int)(G.n - v0 < (uint64_t)TILE_VALUES ? G.n - v0 : (uint64_t)TILE_VALUES);
+  int base = 0;
+
+  if (tile == 0 && lane < 6) {  // codec.py:158, HEADER "<4s4xQd"
+    uint32_t hw;
+    if (lane == 0) hw = 0x31435A47u;  // "GZC1"
+    else if (lane == 1) hw = 0;
+    else if (lane == 2) hw = (uint32_t)G.n;
+    else if (lane == 3) hw = (uint32_t)(G.n >> 32);
+    else {
+      const unsigned long long eb = __double_as_longlong(a.qp.eb);
+      hw = lane == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
+    }
+    reinterpret_cast<uint32_t*>(S.blob)[lane] = hw;
+  }
 
   // ---- 1. fused step: combine the received blob's tile into xs
   if (SRC == SRC_STEP) {
     const uint64_t ts = a.in_tile_off[tile], te = a.in_tile_off[tile + 1];
-    const int base = stage_bytes<false>(stage, a.in_blob + HEADER_BYTES, ts, te, lane);
+    base = stage_bytes<false>(stage, a.in_blob + HEADER_BYTES, ts, te, lane);
     __syncwarp();
     walk_groups(stage, base, (int)(te - ts), a.in_sub_off + tile * GROUPS, nblk, b0, nb, last_cnt, a.st, s_start,
                 s_w, lane);
@@ -377,37 +485,36 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
     decode_row<1>(stage, base, nblk, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, s_start, s_w, lane);
     __syncwarp();
     if (a.acc_out) drain_values(xs, a.acc_out, v0, nval, lane);
+    __syncwarp();
   }
 
-  // ---- 2. closed-loop quantisation, one lane per 32-value block
+  // ---- 2. closed-loop quantisation, one lane per 32-value block; the codes
+  // replace the values in the lane's shared-memory row
   const bool active = lane < nblk;
   const int cnt = active ? ((b0 + lane == nb - 1) ? last_cnt : 32) : 0;
-  uint32_t z[31];
   uint32_t zor = 0;
   int flags = 0;
   float x0 = 0.0f;
   if (active) {
     int fb = FB_SLOW;
-    if (FAST && cnt == 32) fb = fast_block(xs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, z, x0);
+    if (FAST && cnt == 32) fb = fast_block(xs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
     if (fb == FB_SLOW) {  // rare: exact replay of the whole block
       float row[32];
-      load_row(xs, lane, row);
+      if (FAST && cnt == 32) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, s_start, s_w, lane, row);
+      else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
       x0 = row[0];
       uint32_t zl[32];
-      zor = slow_block(row, cnt, a.qp.tw, a.qp.eb, zl, &flags);
-#pragma unroll
-      for (int j = 0; j < 31; ++j) z[j] = zl[j];
+      zor = slow_block(row, cnt, a.qp, zl, &flags);
+      store_codes(xs, lane, x0, zl);
       if (flags & 4) {  // codec.py:83-85: report the first non-finite offset
         for (int j = 0; j < cnt; ++j)
-          if (!isfinite(xs[xs_index(lane, j >> 2) + (j & 3)])) {
+          if (!isfinite(row[j])) {
             atomicMin(&a.st->first_nonfinite, (unsigned long long)(v0 + (uint64_t)lane * 32 + j));
             break;
           }
       }
-    } else {
-      if (fb == FB_RAW) flags |= 2;
-#pragma unroll
-      for (int j = 0; j < 31; j += 3) zor |= z[j] | (j + 1 < 31 ? z[j + 1] : 0u) | (j + 2 < 31 ? z[j + 2] : 0u);
+    } else if (fb == FB_RAW) {
+      flags |= 2;
     }
   }
   const int w = 32 - __clz(zor);                                   // codec.py:224-229
@@ -428,99 +535,267 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   const int tile_bytes = __shfl_sync(0xFFFFFFFFu, incl, 31);
   const int start = incl - size;
 
-  // ---- 4. pack into the staging area; the word straddling two blocks is
-  // completed by the earlier block with the next block's leading bytes
+  // ---- 4. pack into dst; the word straddling two blocks is completed by
+  // the earlier block with the next block's leading bytes
   const uint32_t next_w = __shfl_down_sync(0xFFFFFFFFu, (uint32_t)wbyte, 1);
   const uint32_t next_x0 = __shfl_down_sync(0xFFFFFFFFu, __float_as_uint(x0), 1);
+  uint32_t my_carry = 0;
   if (active) {
     Appender ap;
-    ap.init(stage, start, lane == 0);
+    if (lane == 0 && run_mode) ap.init_carry(dst, pos0, carry);
+    else ap.init(dst, pos0 + start, lane == 0);
+    ap.pol = pol_keep;
     if (raw) {
+      float row[32];
+      reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, s_start, s_w, lane, row);
       ap.append(255ull | ((uint64_t)__float_as_uint(x0) << 8), 5);
       int j = 1;
-      for (; j + 1 < cnt; j += 2) {
-        const float v1 = xs[xs_index(lane, j >> 2) + (j & 3)];
-        const float v2 = xs[xs_index(lane, (j + 1) >> 2) + ((j + 1) & 3)];
-        ap.append((uint64_t)__float_as_uint(v1) | ((uint64_t)__float_as_uint(v2) << 32), 8);
-      }
-      if (j < cnt) ap.append((uint64_t)__float_as_uint(xs[xs_index(lane, j >> 2) + (j & 3)]), 4);
+      for (; j + 1 < cnt; j += 2)
+        ap.append((uint64_t)__float_as_uint(row[j]) | ((uint64_t)__float_as_uint(row[j + 1]) << 32), 8);
+      if (j < cnt) ap.append((uint64_t)__float_as_uint(row[j]), 4);
     } else {
       ap.append((uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8), 5);
-      if (w > 0 && w <= 8) {
-        const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
-        uint32_t pr[16], qd[8];
+      if (w > 0) {
+        uint32_t z[31];
+        load_codes(xs, lane, z);
+        if (w <= 8) {
+          const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
+          const int CB = (ncodes * w + 7) >> 3;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pr[i] = (2 * i + 1 < 31) ? z[2 * i] + z[2 * i + 1] * P1 : z[2 * i];
+          for (int g = 0; g < 4; ++g) {
+            uint32_t pr[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) qd[i] = pr[2 * i] + pr[2 * i + 1] * P2;
-        const int CB = (ncodes * w + 7) >> 3;
+            for (int i = 0; i < 4; ++i) {
+              const int j0 = 8 * g + 2 * i;
+              pr[i] = (j0 + 1 < 31) ? z[j0] + z[j0 + 1] * P1 : z[j0];
+            }
+            const uint32_t qa = pr[0] + pr[1] * P2, qb2 = pr[2] + pr[3] * P2;
+            const uint64_t oct = (uint64_t)qa | ((uint64_t)qb2 << (4 * w));
+            const int L = min(w, CB - g * w);
+            if (L > 0) ap.append(oct, L);
+          }
+        } else {
+          uint64_t acc = 0;
+          int nbits = 0;
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const uint64_t oct = (uint64_t)qd[2 * g] | ((uint64_t)qd[2 * g + 1] << (4 * w));
-          const int L = min(w, CB - g * w);
-          if (L > 0) ap.append(oct, L);
-        }
-      } else if (w > 8) {
-        uint64_t acc = 0;
-        int nbits = 0;
-#pragma unroll
-        for (int j = 0; j < 31; ++j) {
-          if (j < ncodes) {
-            acc |= (uint64_t)z[j] << nbits;
-            nbits += w;
-            if (nbits >= 32) {
-              ap.append(acc & 0xFFFFFFFFull, 4);
-              acc >>= 32;
-              nbits -= 32;
+          for (int j = 0; j < 31; ++j) {
+            if (j < ncodes) {
+              acc |= (uint64_t)z[j] << nbits;
+              nbits += w;
+              if (nbits >= 32) {
+                ap.append(acc & 0xFFFFFFFFull, 4);
+                acc >>= 32;
+                nbits -= 32;
+              }
             }
           }
+          if (nbits > 0) ap.append(acc, (nbits + 7) >> 3);
         }
-        if (nbits > 0) ap.append(acc, (nbits + 7) >> 3);
       }
     }
-    const uint64_t lead = (lane + 1 < nblk) ? ((uint64_t)next_w | ((uint64_t)next_x0 << 8)) : 0ull;
-    ap.finish(lead);
+    if (lane + 1 < nblk) ap.finish((uint64_t)next_w | ((uint64_t)next_x0 << 8));
+    else if (!run_mode) ap.finish(0ull);
+    else my_carry = ap.pend;  // the run's next tile completes this word
   }
+  carry = __shfl_sync(0xFFFFFFFFu, my_carry, nblk > 0 ? nblk - 1 : 0);
   // sub-offsets (final values, independent of the tile's position)
   const int st8 = __shfl_sync(0xFFFFFFFFu, start, (lane & 3) * GROUP);
   if (lane < GROUPS && S.out_sub_off) S.out_sub_off[tile * GROUPS + lane] = (uint16_t)(lane * GROUP < nblk ? st8 : tile_bytes);
-  if (active && a.blk_off) a.blk_off[b0 + lane] = (unsigned long long)start;  // made absolute in pass B
-  __syncwarp();
+  if (active && a.blk_off) a.blk_off[b0 + lane] = (unsigned long long)start;  // made absolute in phase B
   return tile_bytes;
 }
 
-// Persistent encoder, one kernel, two phases per CTA:
-//   A. each warp encodes a contiguous run of tiles (prefetching the next
-//      tile with cp.async while quantising the current one) and appends the
-//      packed bytes to its run in a local scratch buffer (stays in L2);
-//   B. the CTA publishes its total, sums the totals of all earlier CTAs of the
-//      segment (the exclusive scan of codec.py:241-243 at CTA granularity,
-//      one round trip), then every warp copies its run to its final place in
-//      the blob -- which may be a peer GPU's memory (the NVLink send).
-// CTA ids come from an atomic ticket, so a CTA only ever waits for CTAs that
-// are already running.
+// Warp-cooperative copy of `len` bytes from 16-byte aligned `src` to any
+// `dst` (possibly a peer GPU): each lane produces whole aligned 16-byte
+// destination chunks from two source chunks; loads are batched so that
+// several round trips are in flight per lane.  Edge bytes are written
+// byte-wise (shared with neighbouring ranges).
+__device__ __forceinline__ void copy_run(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint64_t len, int lane) {
+  if (!len) return;
+  const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + len;
+  const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cl = E & ~(uintptr_t)15;
+  if (cf >= cl) {
+    for (uint64_t i = lane; i < len; i += 32) dst[i] = src[i];
+    return;
+  }
+  const uint64_t head = cf - A, nch = (cl - cf) >> 4;
+  const int sh = (int)(head & 3) * 8, wo = (int)(head >> 2) & 3;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + (head & ~(uint64_t)15));
+  uint4* d4 = reinterpret_cast<uint4*>(cf);
+  constexpr int B = 4;
+  for (uint64_t c0 = lane; c0 < nch; c0 += 32 * B) {
+    uint4 lo[B], hi[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint64_t c = c0 + 32 * b;
+      if (c < nch) {
+        lo[b] = __ldcs(s4 + c);
+        hi[b] = __ldcs(s4 + c + 1);
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      const uint64_t c = c0 + 32 * b;
+      if (c < nch) {
+        const uint4 cur = lo[b], nxt = hi[b];
+        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+        uint4 o;
+        o.x = __funnelshift_r(a0, a1, sh);
+        o.y = __funnelshift_r(a1, a2, sh);
+        o.z = __funnelshift_r(a2, a3, sh);
+        o.w = __funnelshift_r(a3, a4, sh);
+        d4[c] = o;
+      }
+    }
+  }
+  const int tail = (int)(E - cl);
+  if ((uint64_t)lane < head) dst[lane] = src[lane];
+  if (lane >= 16 && lane - 16 < tail) dst[len - tail + (lane - 16)] = src[len - tail + (lane - 16)];
+}
+
+// Lane-per-tile copy with batched loads: `len` bytes from a 16-byte aligned
+// slot to any destination (possibly a peer GPU); byte stores for the ragged
+// edges (shared with neighbouring tiles, hence byte-wise), aligned 16-byte
+// stores in between, eight source chunks in flight per batch.
+__device__ __forceinline__ void lane_copy_batched(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int len) {
+  if (len <= 0) return;
+  const int h = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+  for (int i = 0; i < h; ++i) dst[i] = src[i];
+  const int nch = (len - h) >> 4;
+  const uint4* s4 = reinterpret_cast<const uint4*>(src + (h & ~15));
+  uint4* d4 = reinterpret_cast<uint4*>(dst + h);
+  const int wo = (h >> 2) & 3, sh = (h & 3) * 8;
+  constexpr int B = 8;
+  for (int c0 = 0; c0 < nch; c0 += B) {
+    uint4 v[B + 1];
+#pragma unroll
+    for (int b = 0; b <= B; ++b)
+      if (c0 + b <= nch) v[b] = __ldcs(s4 + c0 + b);
+#pragma unroll
+    for (int b = 0; b < B; ++b) {
+      if (c0 + b < nch) {
+        const uint4 cur = v[b], nxt = v[b + 1];
+        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+        uint4 o;
+        o.x = __funnelshift_r(a0, a1, sh);
+        o.y = __funnelshift_r(a1, a2, sh);
+        o.z = __funnelshift_r(a2, a3, sh);
+        o.w = __funnelshift_r(a3, a4, sh);
+        d4[c0 + b] = o;
+      }
+    }
+  }
+  for (int i = h + 16 * nch; i < len; ++i) dst[i] = src[i];
+}
+
+// Warp-cooperative copy of up to 4 tiles at once (coalesced): tile i has
+// `len[i]` bytes in a 16-byte aligned slot `src[i]` and goes to `dst[i]`
+// (any alignment, possibly a peer GPU).  Lane l produces aligned destination
+// chunk l (+32, +64, ... for long tiles) from source chunks l and l+1; all
+// loads of the group are issued before the stores.  Edge bytes are written
+// byte-wise (they share 16-byte chunks with neighbouring tiles).
+__device__ __forceinline__ void warp_copy4(uint8_t* const (&dst)[4], const uint8_t* const (&src)[4], const int (&len)[4],
+                                           int lane) {
+  int head[4], nch[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    head[i] = min(len[i], (int)((16 - (reinterpret_cast<uintptr_t>(dst[i]) & 15)) & 15));
+    nch[i] = len[i] > head[i] ? (len[i] - head[i]) >> 4 : 0;
+  }
+  const int maxch = max(max(nch[0], nch[1]), max(nch[2], nch[3]));
+  for (int c0 = 0; c0 < maxch; c0 += 32) {
+    const int cc = c0 + lane;
+    uint4 lo[4], hi[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (cc < nch[i]) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src[i] + (head[i] & ~15));
+        lo[i] = __ldcs(s4 + cc);
+        hi[i] = __ldcs(s4 + cc + 1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (cc < nch[i]) {
+        const int h = head[i], wo = (h >> 2) & 3, sh = (h & 3) * 8;
+        const uint4 cur = lo[i], nxt = hi[i];
+        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+        uint4 o;
+        o.x = __funnelshift_r(a0, a1, sh);
+        o.y = __funnelshift_r(a1, a2, sh);
+        o.z = __funnelshift_r(a2, a3, sh);
+        o.w = __funnelshift_r(a3, a4, sh);
+        reinterpret_cast<uint4*>(dst[i] + h)[cc] = o;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int tail0 = head[i] + 16 * nch[i];
+    if (lane < head[i]) dst[i][lane] = src[i][lane];
+    for (int b = tail0 + lane; b < len[i]; b += 32) dst[i][b] = src[i][b];
+  }
+}
+
+// Encoder (one launch, one CTA per SM, no grid-wide barrier).
+//   A. CTA c owns a contiguous tile range of one segment (CTAs are split over
+//      segments in proportion to their tiles; c is an atomic ticket, so a CTA
+//      only ever waits for CTAs that are running).  Its warps claim tiles of
+//      the range from a shared-memory counter -- warps of one SM do not get
+//      equal issue slots, so the work must be balanced dynamically -- and
+//      prefetch the next claimed tile (cp.async, L2 evict_first) while they
+//      quantise the current one.  Each tile is packed into its own aligned
+//      scratch slot (L2 evict_last).
+//   B. The CTA publishes its byte total and sums the totals of the segment's
+//      earlier CTAs (the exclusive scan of codec.py:241-243 as a decoupled
+//      prefix), scans its tiles' sizes, and copies every slot to its final
+//      offset -- possibly in a peer GPU's memory (the NVLink send of a fused
+//      reduce-scatter step) -- one lane per tile, then drops the slots from L2.
 template <int SRC, int NSEG, bool FAST>
-__global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_encode(const EncodeArgs<NSEG> a) {
+__global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const EncodeArgs<NSEG> a) {
+  constexpr int NW = enc_warps(SRC);
+  constexpr int NT = 32 * NW;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
-  __shared__ uint16_t s_start[SRC == SRC_STEP ? WARPS : 1][TB];
-  __shared__ uint8_t s_w[SRC == SRC_STEP ? WARPS : 1][TB];
-  __shared__ unsigned long long s_cta, s_gen, s_base;
-  __shared__ unsigned long long s_wtot[WARPS];
-  __shared__ unsigned long long s_red[CTA_THREADS / 32];
+  __shared__ uint16_t s_start[SRC == SRC_STEP ? NW : 1][TB];
+  __shared__ uint8_t s_w[SRC == SRC_STEP ? NW : 1][TB];
+  __shared__ unsigned long long s_cta, s_gen, s_base, s_carry;
+  __shared__ unsigned int s_next;
+  __shared__ unsigned long long s_red[NW];
+  __shared__ unsigned long long s_off[NT];
+  __shared__ uint32_t s_sz[NT];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned char* my = smem + warp * ENC_WARP_SMEM;
+  constexpr int WSMEM = SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4;
+  unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
   float* xsb1 = reinterpret_cast<float*>(my + TILE_VALUES * 4);
-  uint32_t* stage = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);
+  uint32_t* stage = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);  // fused step only
   TileWs* ws = a.ws;
+  const int wi = SRC == SRC_STEP ? warp : 0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
   if (tid == 0) {
     s_cta = atomicAdd(&ws->ticket, 1ull);
     s_gen = ld_volatile_u64(&ws->gen);
+    s_next = 0;
   }
   __syncthreads();
   const unsigned long long c = s_cta, gen = s_gen;
+  const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
+  const unsigned long long ts0 = gtimer();
+
+  // ---- this CTA's segment and tile range
   int k = 0;
   if (NSEG > 1) {
 #pragma unroll 1
@@ -528,107 +803,165 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_encode(const EncodeArgs
       if (a.seg[i].cta_base <= c) k = i;
   }
   const Seg& S = a.seg[k];
-  const uint64_t cta_end = (k + 1 < a.nseg) ? a.seg[k + 1].cta_base : a.nctas;
-  const uint64_t ncta = cta_end - S.cta_base, cl = c - S.cta_base;
+  const uint64_t cta_lo = S.cta_base, cta_hi = (k + 1 < a.nseg) ? a.seg[k + 1].cta_base : a.nctas;
+  const uint64_t cl = c - cta_lo, ncta = cta_hi - cta_lo;
   const SegGeom G = seg_geom(S.n);
-  // contiguous tile run of this CTA, then of this warp
-  const uint64_t per_cta = (G.ntiles + ncta - 1) / ncta;
-  const uint64_t c0 = umin64(cl * per_cta, G.ntiles), c1 = umin64(c0 + per_cta, G.ntiles);
-  const uint64_t per_warp = (c1 - c0 + WARPS - 1) / WARPS;
-  const uint64_t t0 = umin64(c0 + warp * per_warp, c1), t1 = umin64(t0 + per_warp, c1);
-  uint8_t* run_base = a.scratch + (S.tile_base + t0) * (uint64_t)TILE_SLOT;
-  uint32_t* rel = a.tile_rel + S.tile_base;
+  const uint64_t r0 = (G.ntiles * cl) / ncta, r1 = (G.ntiles * (cl + 1)) / ncta;
+  const unsigned int nr = (unsigned int)(r1 - r0);
+  uint32_t* const sizes = a.tile_rel + S.tile_base;
+  uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
 
-  if (cl == 0 && warp == 0 && lane < 6) {  // codec.py:158, HEADER "<4s4xQd"
-    uint32_t hw;
-    if (lane == 0) hw = 0x31435A47u;  // "GZC1"
-    else if (lane == 1) hw = 0;
-    else if (lane == 2) hw = (uint32_t)G.n;
-    else if (lane == 3) hw = (uint32_t)(G.n >> 32);
-    else {
-      const unsigned long long eb = __double_as_longlong(a.qp.eb);
-      hw = lane == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
-    }
-    reinterpret_cast<uint32_t*>(S.blob)[lane] = hw;
-  }
-  if (SRC == SRC_STEP) __syncthreads();
-
-  // ---- phase A: encode the warp's run into scratch
-  unsigned long long run = 0;
-  if (t0 < t1) {
-    const uint64_t nv0 = G.n - t0 * TILE_VALUES;
-    prefetch_values(xsb0, S.x, t0 * TILE_VALUES, (int)umin64(nv0, TILE_VALUES), lane);
-  }
+  // ---- phase A: warps claim tiles of [r0, r1) dynamically
+  auto claim = [&]() -> unsigned int {
+    unsigned int v = 0;
+    if (lane == 0) v = atomicAdd(&s_next, 1u);
+    return __shfl_sync(0xFFFFFFFFu, v, 0);
+  };
+  unsigned int j = claim();
+  unsigned int j1 = j < nr ? claim() : nr;
+  if (j < nr) prefetch_tile(a, S.tile_base + r0 + j, xsb0, lane, pol_in);
   int buf = 0;
-  for (uint64_t t = t0; t < t1; ++t) {
-    if (t + 1 < t1) {
-      const uint64_t v1 = (t + 1) * TILE_VALUES;
-      prefetch_values(buf ? xsb0 : xsb1, S.x, v1, (int)umin64(G.n - v1, TILE_VALUES), lane);
-    } else {
-      cp_async_commit();
-    }
+  unsigned long long wait_ns = 0, ndone = 0;
+  uint32_t dummy = 0;
+  while (j < nr) {
+    prefetch_tile(a, j1 < nr ? S.tile_base + r0 + j1 : a.total_tiles, buf ? xsb0 : xsb1, lane, pol_in);
+    const unsigned long long tw0 = a.dbg ? gtimer() : 0;
     cp_async_wait_1();
     __syncwarp();
-    const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0, stage, s_start[SRC == SRC_STEP ? warp : 0],
-                                                s_w[SRC == SRC_STEP ? warp : 0], s_step, lane);
-    if (lane == 0) rel[t] = (uint32_t)run;
-    stage_to_scratch(run_base, run, stage, tb, lane);
-    run += (unsigned long long)tb;
+    if (a.dbg) wait_ns += gtimer() - tw0;
+    const uint64_t t = r0 + j;
+    const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
+                                                reinterpret_cast<uint32_t*>(slots + t * (uint64_t)TILE_SLOT), 0, false,
+                                                dummy, stage, s_start[wi], s_w[wi], s_step, pol_keep, lane);
+    if (lane == 0) sizes[t] = (uint32_t)tb;
+    ++ndone;
     __syncwarp();
     buf ^= 1;
+    j = j1;
+    j1 = j < nr ? claim() : nr;
   }
-  if (lane == 0) s_wtot[warp] = run;
-  __syncthreads();
+  cp_async_wait_all();
+  const unsigned long long ts1 = gtimer();
+  __syncthreads();  // every tile of the range is in its slot, sizes written
 
-  // ---- phase B: CTA prefix over the segment's earlier CTAs
+  // ---- phase B: CTA total, decoupled prefix over earlier CTAs
+  unsigned long long tot = 0;
+  for (unsigned int q = tid; q < nr; q += NT) tot += sizes[r0 + q];
+  tot = warp_sum_u64(tot);
+  if (lane == 0) s_red[warp] = tot;
+  __syncthreads();
   if (tid == 0) {
-    unsigned long long tot = 0;
+    unsigned long long t2 = 0;
 #pragma unroll
-    for (int j = 0; j < WARPS; ++j) tot += s_wtot[j];
-    st_volatile_u64(&ws->status[c], mk_status(gen, 1u, tot));
+    for (int q = 0; q < NW; ++q) t2 += s_red[q];
+    s_carry = t2;
+    st_volatile_u64(&ws->status[c], mk_status(gen, 1u, t2));
   }
   unsigned long long part = 0;
-  for (uint64_t p = S.cta_base + tid; p < c; p += CTA_THREADS) {
+  for (uint64_t p = cta_lo + tid; p < c; p += NT) {
     unsigned long long sw;
     while (true) {
       sw = ld_volatile_u64(&ws->status[p]);
       if (((sw >> 48) & 0xFFFF) == (gen & 0xFFFF) && ((sw >> 46) & 3) != 0) break;
-      __nanosleep(64);
+      __nanosleep(32);
     }
     part += sw & VALUE_MASK;
   }
+  __syncthreads();  // s_red reuse
   part = warp_sum_u64(part);
   if (lane == 0) s_red[warp] = part;
   __syncthreads();
   if (tid == 0) {
     unsigned long long b = 0;
 #pragma unroll
-    for (int j = 0; j < CTA_THREADS / 32; ++j) b += s_red[j];
+    for (int q = 0; q < NW; ++q) b += s_red[q];
     s_base = b;
   }
   __syncthreads();
-  unsigned long long base = s_base;
+  const unsigned long long ts2 = gtimer();
+
+  // ---- phase B: block-wide scan of the range's tile sizes; each warp copies
+  // the 32 tiles its lanes own, four at a time (coalesced, loads batched)
+  unsigned long long run = s_base;
+  for (unsigned int q0 = 0; q0 < nr; q0 += NT) {
+    const unsigned int q = q0 + tid;
+    const unsigned long long sz = q < nr ? sizes[r0 + q] : 0ull;
+    unsigned long long incl = sz;
 #pragma unroll
-  for (int j = 0; j < WARPS; ++j) base += j < warp ? s_wtot[j] : 0ull;
-
-  // ---- phase B: copy the run to its final place; tile offsets, length
-  copy_to_unaligned(S.blob + HEADER_BYTES + base, run_base, run, lane);
-  for (uint64_t t = t0 + lane; t < t1; t += 32) {
-    if (S.out_tile_off) S.out_tile_off[t] = base + rel[t];
+    for (int d = 1; d < 32; d <<= 1) {
+      const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+      if (lane >= d) incl += v;
+    }
+    __syncthreads();
+    if (lane == 31) s_red[warp] = incl;
+    __syncthreads();
+    unsigned long long wpre = 0, rtot = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) {
+      wpre += w2 < warp ? s_red[w2] : 0ull;
+      rtot += s_red[w2];
+    }
+    const unsigned long long o = run + wpre + incl - sz;
+    if (q < nr) {
+      const uint64_t t = r0 + q;
+      if (S.out_tile_off) S.out_tile_off[t] = o;
+      if (a.blk_off && k == 0) {
+        const uint64_t bb0 = t * TB, bb1 = umin64(bb0 + TB, G.nb);
+        for (uint64_t b = bb0; b < bb1; ++b) a.blk_off[b] += o;
+      }
+    }
+    if (q < nr) {
+      s_off[tid] = o;
+      s_sz[tid] = (uint32_t)sz;
+    }
+    __syncthreads();
+    // tiles of this round are spread over all warps: warp w copies w, w+NW, ...
+    const unsigned int cnt = (unsigned int)min((unsigned long long)NT, (unsigned long long)(nr - q0));
+    for (unsigned int r = warp; r < cnt; r += 4 * NW) {
+      uint8_t* dsts[4];
+      const uint8_t* srcs[4];
+      int lens[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const unsigned int rr = r + i * NW;
+        const bool v = rr < cnt;
+        const unsigned int rc = v ? rr : r;
+        dsts[i] = S.blob + HEADER_BYTES + s_off[rc];
+        srcs[i] = slots + (r0 + q0 + rc) * (uint64_t)TILE_SLOT;
+        lens[i] = v ? (int)s_sz[rc] : 0;
+      }
+      warp_copy4(dsts, srcs, lens, lane);
+    }
+    __syncthreads();
+    run += rtot;
   }
-  if (a.blk_off && k == 0) {
-    for (uint64_t b = t0 * TB + lane; b < umin64(t1 * TB, G.nb); b += 32) a.blk_off[b] += base + rel[b / TB];
+  const unsigned long long tb3 = gtimer();
+  // the segment's last CTA knows the total: blob length and end offset
+  if (c == cta_hi - 1 && tid == 0) {
+    const unsigned long long total = s_base + s_carry;
+    if (S.out_tile_off) S.out_tile_off[G.ntiles] = total;
+    *S.out_len = HEADER_BYTES + total;
+    if (G.ntiles == 0) {  // empty blob: header only (codec.py:159-160)
+      uint32_t* hb = reinterpret_cast<uint32_t*>(S.blob);
+      const unsigned long long eb = __double_as_longlong(a.qp.eb);
+      hb[0] = 0x31435A47u;
+      hb[1] = 0;
+      hb[2] = 0;
+      hb[3] = 0;
+      hb[4] = (uint32_t)eb;
+      hb[5] = (uint32_t)(eb >> 32);
+    }
   }
-  if (lane == 0 && t0 < t1 && t1 == G.ntiles) {
-    if (S.out_tile_off) S.out_tile_off[G.ntiles] = base + run;
-    *S.out_len = HEADER_BYTES + base + run;
+  if (a.dbg && lane == 0) {  // experiments: per-warp timestamps
+    unsigned long long* d = a.dbg + (c * NW + warp) * 12;
+    d[0] = ts0; d[1] = ts1; d[2] = ts2; d[3] = gtimer(); d[4] = ndone;
+    d[5] = wait_ns; d[6] = c; d[7] = tb3; d[8] = tb3; d[9] = tb3;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    d[10] = smid;
+    d[11] = ndone;
   }
-  if (tid == 0 && G.ntiles == 0 && cl == 0) {
-    if (S.out_tile_off) S.out_tile_off[0] = 0;
-    *S.out_len = HEADER_BYTES;
-  }
-
-  // retire: the last CTA to finish resets the tickets and bumps gen
+  // retire: the last CTA resets the ticket and bumps gen
   __syncthreads();
   if (tid == 0) {
     __threadfence();

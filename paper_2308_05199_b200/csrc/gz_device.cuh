@@ -53,12 +53,13 @@ constexpr int MAGIC32_BITS = 0x4B400000;
 // advances when the last CTA of a launch retires, so no per-launch memset is
 // needed and CUDA-graph replay is safe.
 constexpr int MAXGRID = 4096;
-constexpr int TILE_SLOT = 4160;  // scratch bytes reserved per tile (>= 32 * 129, 16-aligned)
+constexpr int TILE_SLOT = 4224;  // scratch bytes reserved per tile (>= 32 * 129, 128-aligned)
 struct TileWs {
-  unsigned long long ticket;
-  unsigned long long done;
+  unsigned long long ticket;        // dynamic tile tickets (own 128-byte line)
+  unsigned long long pad0[15];
+  unsigned long long done;          // retire counter (own line)
   unsigned long long gen;
-  unsigned long long pad;
+  unsigned long long pad1[14];
   unsigned long long status[MAXGRID];
 };
 
@@ -132,16 +133,38 @@ __device__ __noinline__ StepOut slow_step(float prev32, float x, double tw, doub
 // partial final block, for blocks the fast pass could not prove, and for all
 // blocks when eb lies outside the fast path's range.  Returns the zigzag OR
 // and ORs overflow / error / non-finite flags into *flags.
-__device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, double tw, double eb, uint32_t* z,
+__device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, const QParams P, uint32_t* z,
                                             int* flags) {
+  // Step by step: the proven fast decision where it applies (see fast_block),
+  // the verbatim reference arithmetic (slow_step) where it does not.
   float prev32 = xs_row_vals[0];
   int f = isfinite(prev32) ? 0 : 4;
   uint32_t zor = 0;
   for (int j = 1; j < cnt; ++j) {
-    const StepOut o = slow_step(prev32, xs_row_vals[j], tw, eb);
-    prev32 = o.rec;
-    f |= o.flags;
-    const uint32_t zz = ((uint32_t)o.code << 1) ^ (uint32_t)(o.code >> 31);
+    const float x = xs_row_vals[j];
+    int code;
+    bool done = false;
+    if (P.fast) {
+      const float vf = __fmul_rn(__fsub_rn(x, prev32), P.rtw);
+      const float m = __fadd_rn(vf, MAGIC32);
+      const float fr = __fsub_rn(vf, __fsub_rn(m, MAGIC32));
+      if (fmaf(fabsf(vf), 0x1p-21f, fabsf(fr)) < P.thr) {
+        code = __float_as_int(m) - MAGIC32_BITS;
+        const double t = __dadd_rn((double)prev32, __dmul_rn(i32_to_f64(code), P.tw));
+        prev32 = __double2float_rn(t);
+        const float e = fabsf(__fsub_rn(prev32, x));
+        if (e > P.ehi) f |= 2;
+        else if (e >= P.elo && fabs(__dsub_rn((double)prev32, (double)x)) > P.eb) f |= 2;
+        done = true;
+      }
+    }
+    if (!done) {
+      const StepOut o = slow_step(prev32, x, P.tw, P.eb);
+      prev32 = o.rec;
+      f |= o.flags;
+      code = o.code;
+    }
+    const uint32_t zz = ((uint32_t)code << 1) ^ (uint32_t)(code >> 31);
     z[j - 1] = zz;
     zor |= zz;
   }
@@ -170,13 +193,19 @@ __device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, d
 //   (>= eb (1 + 2^-22)) proves |rec - x| > eb; only e in [elo, ehi] is undecided.
 enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
 
-__device__ __forceinline__ int fast_block(const float* xs, int row, double tw, float rtw, float thr, float elo,
-                                          float ehi, uint32_t (&z)[31], float& x0) {
+__device__ __forceinline__ int fast_block(float* xs, int row, double tw, float rtw, float thr, float elo, float ehi,
+                                          uint32_t& zor_out, float& x0) {
+  // The codes overwrite the consumed values in place: slot j of the row
+  // receives code j-1 (slot 0 keeps x0), one 16-byte store per 4 steps.
   float4 c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, 0));
   float prev32 = c4.x;
   x0 = c4.x;
   double prev64 = (double)prev32;
-  bool rnd = true, ge = false, gt = false;
+  bool rnd = true;
+  float emax = 0.0f;  // max |rec - x| over the block (f32, decided once)
+  uint32_t zor = 0;
+  uint32_t zc[4];
+  zc[0] = __float_as_uint(x0);
 #pragma unroll
   for (int j = 1; j < 32; ++j) {
     if ((j & 3) == 0) c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, j >> 2));
@@ -191,13 +220,36 @@ __device__ __forceinline__ int fast_block(const float* xs, int row, double tw, f
     prev32 = __double2float_rn(t);
     prev64 = (double)prev32;
     const float e = fabsf(__fsub_rn(prev32, x));
-    ge |= e >= elo;
-    gt |= e > ehi;
-    z[j - 1] = ~((qb << 1) ^ (uint32_t)((int)qb >> 31));            // zigzag(q)
+    emax = fmaxf(emax, e);
+    const uint32_t z = ~((qb << 1) ^ (uint32_t)((int)qb >> 31));     // zigzag(q)
+    zor |= z;
+    zc[j & 3] = z;
+    if ((j & 3) == 3)
+      *reinterpret_cast<uint4*>(xs + xs_index(row, j >> 2)) = make_uint4(zc[0], zc[1], zc[2], zc[3]);
   }
+  zor_out = zor;
   if (!rnd) return FB_SLOW;
-  if (gt) return FB_RAW;
-  return ge ? FB_SLOW : FB_PACKED;
+  if (emax > ehi) return FB_RAW;             // some error provably > eb
+  return emax >= elo ? FB_SLOW : FB_PACKED;  // undecided within 2^-22 of eb
+}
+
+// code j (0..30) of a row written by fast_block / store_codes
+__device__ __forceinline__ void load_codes(const float* xs, int row, uint32_t (&z)[31]) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint4 v = *reinterpret_cast<const uint4*>(xs + xs_index(row, c));
+    if (c > 0) z[4 * c - 1] = v.x;
+    z[4 * c + 0] = v.y;
+    z[4 * c + 1] = v.z;
+    if (4 * c + 2 < 31) z[4 * c + 2] = v.w;
+  }
+}
+__device__ __forceinline__ void store_codes(float* xs, int row, float x0, const uint32_t* z) {
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const uint32_t a = c ? z[4 * c - 1] : __float_as_uint(x0);
+    *reinterpret_cast<uint4*>(xs + xs_index(row, c)) = make_uint4(a, z[4 * c], z[4 * c + 1], z[4 * c + 2]);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -205,8 +257,13 @@ __device__ __forceinline__ int fast_block(const float* xs, int row, double tw, f
 // exactly the words whose first byte lies in its block; the last such word is
 // completed with the first bytes of the next block ([w][x0...]), so no two
 // threads ever store the same word and no atomics are needed.
+__device__ __forceinline__ void st_u32_hint(uint32_t* p, uint32_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.b32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+
 struct Appender {
-  uint32_t* stage;
+  uint32_t* stage;  // global memory (a scratch run or slot)
+  uint64_t pol;     // L2 policy of the stores
   int wi;          // word index of the pending word
   uint32_t pend;   // pending bytes (low npend bytes valid)
   int npend;
@@ -218,8 +275,17 @@ struct Appender {
     pend = 0;
     skip = (npend != 0) && !owns_first;
   }
+  // first block of a tile appended to a run: the previous tile left its last
+  // partial word as `carry` (low byte_pos & 3 bytes valid)
+  __device__ __forceinline__ void init_carry(uint32_t* s, int byte_pos, uint32_t carry) {
+    stage = s;
+    wi = byte_pos >> 2;
+    npend = byte_pos & 3;
+    pend = npend ? carry : 0u;
+    skip = false;
+  }
   __device__ __forceinline__ void put(uint32_t w) {
-    if (!skip) stage[wi] = w;
+    if (!skip) st_u32_hint(stage + wi, w, pol);
     skip = false;
     ++wi;
   }
