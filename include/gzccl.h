@@ -117,6 +117,21 @@ int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value);
 /* copy `*d_len + tail` bytes determined on the device: dst may be a peer */
 int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64_t max_bytes, gz_stream_t stream);
 
+/* Forward a set of byte ranges in ONE launch (a binomial-scatter hop: the
+ * child pulls its subtree's blobs, sidecars and lengths from its parent,
+ * collectives.py:511-525).  Item i copies min(*d_len, max_bytes) bytes when
+ * d_len is non-NULL (a blob whose length is known only on the device), else
+ * max_bytes.  src/dst may be peer (IPC) pointers; 16-byte aligned items
+ * move as 16-byte words, others byte by byte. */
+typedef struct {
+  const uint8_t* src;
+  uint8_t* dst;
+  const uint64_t* d_len;
+  uint64_t max_bytes;
+} gz_copy_item;
+#define GZ_MAX_COPY_ITEMS 64
+int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

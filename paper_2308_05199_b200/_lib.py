@@ -43,6 +43,7 @@ SIGNATURES = {
     "gz_stream_write_u32": (i32, [p, p, u32]),
     "gz_stream_wait_u32_geq": (i32, [p, p, u32]),
     "gz_copy_blob": (i32, [p, p, p, u64, p]),
+    "gz_copy_items": (i32, [p, u32, p]),
 }
 
 _lib = None

@@ -100,6 +100,7 @@ class Communicator:
         self._peer = None
         self.last_compression_ratio = None
         self.launches_per_call = 0
+        self.events = None  # list -> (label, cuda event) marks after every wait/launch (profiling)
 
     # ------------------------------------------------------------------ setup
     def _setup(self, n: int):
@@ -141,6 +142,7 @@ class Communicator:
         self._peer = None
         self._buf = None
         self._n = None
+        _scatter_close(self)
 
     def close(self):
         try:
@@ -164,6 +166,13 @@ class Communicator:
 
     def _wait(self, off: int, value: int, s: int):
         L.check(L.lib().gz_stream_wait_u32_geq(s, self._addr(self.rank, off), value), "gz_stream_wait_u32_geq")
+        self._mark("wait")
+
+    def _mark(self, label: str):
+        if self.events is not None:
+            ev = torch.cuda.Event(enable_timing=True)
+            ev.record(self.stream)
+            self.events.append((label, ev))
 
     # ------------------------------------------------------------ allreduce
     def ring_allreduce(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
@@ -205,6 +214,7 @@ class Communicator:
             return self._addr(r, b), self._addr(r, sc)
 
         launches = 0
+        self._mark("start")
         # the right neighbour must have consumed our previous writes
         if self.epoch:
             self._wait(lay.rs_consumed(), self.epoch, s)
@@ -216,6 +226,7 @@ class Communicator:
                                         self._addr(p.dst, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
                                         tws.numel(), ws.status_ptr(), s), "gz_compress")
                 launches += 1
+                self._mark("compress")
                 self._signal(p.dst, lay.rs_full(p.slot), e, s)
             elif isinstance(p, Reduce):
                 # fused decompress(recv) + op + compress; the output stores are the send
@@ -238,6 +249,7 @@ class Communicator:
                                            lay.blob_cap, olen, osc, tws.data_ptr(), tws.numel(), ws.status_ptr(), s),
                         "gz_reduce_step")
                 launches += 1
+                self._mark("reduce_last" if p.last else "reduce")
                 if not p.last:
                     self._signal(p.dst, lay.rs_full(p.slot + 1), e, s)
                 else:
@@ -254,6 +266,7 @@ class Communicator:
                                                   chunk_ptr(out, p.chunk), ws.status_ptr(), s),
                         "gz_decompress_sidecar")
                 launches += 1
+                self._mark("decode")
                 self._signal(p.owner, lay.ag_consumed(i), e, s)
         self.epoch = e
         self.launches_per_call = launches
@@ -269,3 +282,195 @@ class Communicator:
         m = self.spans[c][1] - self.spans[c][0]
         self.last_compression_ratio = round(4 * m / ln, 4) if ln else None
         return self.last_compression_ratio
+
+
+
+class _CopyItem(ctypes.Structure):
+    _fields_ = [("src", ctypes.c_void_p), ("dst", ctypes.c_void_p), ("d_len", ctypes.c_void_p),
+                ("max_bytes", ctypes.c_uint64)]
+
+
+class _ScatterLayout:
+    """One IPC buffer per rank, same layout everywhere: flags, lengths, and a
+    worst-case slot (blob + sidecar) per VIRTUAL rank, so a tree hop's range
+    [lo, hi) is the same offsets on the parent and the child."""
+
+    def __init__(self, world: int, vcounts):
+        lib = L.lib()
+        self.world = world
+        off = _al(4 * (1 + world))  # u32 flags: ready, consumed[world]
+        self.len_off = off
+        off += _al(8 * world)
+        self.slot, self.sc, self.cap, self.sc_bytes = [], [], [], []
+        for c in vcounts:
+            self.slot.append(off)
+            self.cap.append(int(lib.gz_compress_bound(c)))
+            off += _al(self.cap[-1])
+            self.sc.append(off)
+            self.sc_bytes.append(int(lib.gz_sidecar_bytes(c)))
+            off += _al(self.sc_bytes[-1])
+        self.total = off
+
+    READY = 0
+
+    @staticmethod
+    def consumed(j):
+        return 4 * (1 + j)
+
+
+def _open_peers(comm, buf):
+    lib = L.lib()
+    hsz = lib.gz_ipc_handle_size()
+    h = (ctypes.c_char * hsz)()
+    L.check(lib.gz_ipc_get_handle(buf.data_ptr(), h), "gz_ipc_get_handle")
+    handles = [None] * comm.world
+    dist.all_gather_object(handles, bytes(h), group=comm.group)
+    peers = []
+    for r, hb in enumerate(handles):
+        if r == comm.rank:
+            peers.append(buf.data_ptr())
+        else:
+            ptr = ctypes.c_void_p()
+            L.check(lib.gz_ipc_open_handle(ctypes.create_string_buffer(hb, hsz), ctypes.byref(ptr)), "gz_ipc_open_handle")
+            peers.append(ptr.value)
+    return peers
+
+
+def _scatter_close(self):
+    peers = getattr(self, "_sc_peer", None)
+    if peers is not None:
+        lib = L.lib()
+        torch.cuda.synchronize(self.device)
+        for r, p in enumerate(peers):
+            if r != self.rank and p:
+                lib.gz_ipc_close(p)
+    self._sc_peer = None
+    self._sc_buf = None
+    self._sc_key = None
+
+
+def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: str = "tree", out=None):
+    """This rank's part of binomial_scatter_c (collectives.py:467-532).
+
+    The root passes its whole buffer ``x`` (other ranks: None); every rank
+    returns its ``counts[rank]`` values — the root its slice verbatim, the
+    others their block decoded from the root's compress-once blob.
+
+    * the root compresses all N blocks in virtual-rank order in ONE launch
+      (gz_compress_segments = compress_blocks, codec.py:408-427);
+    * routing="tree": each rank pulls its subtree's range [vr, vr+extent) of
+      blobs + sidecars + lengths from its tree parent in one gz_copy_items
+      launch (the reference's byte-range forwarding, collectives.py:511-525),
+      then signals its children; routing="direct": every rank decodes its blob
+      straight out of the root's memory (same bytes, same output — on NVSwitch
+      all peers are one hop away);
+    * the size table never travels separately: lengths sit next to the blobs
+      and the sidecar carries the block offsets.
+    """
+    from .schedule import scatter_route
+
+    if routing not in ("tree", "direct"):
+        raise ValueError(f"unknown routing {routing!r}")
+    ebf = _check_eb(eb)
+    N, me = self.world, self.rank
+    if not 0 <= root < N:
+        raise ValueError(f"root {root} out of range [0, {N})")
+    meta = None
+    if me == root:
+        # validated at the root, the verdict broadcast so every rank raises alike
+        try:
+            if not isinstance(x, torch.Tensor) or x.dim() != 1 or x.dtype != torch.float32 or not x.is_cuda:
+                raise ValueError("root buffer must be a flat 1-D float32 CUDA tensor")
+            meta = [int(x.numel())] + scatter_counts(int(x.numel()), N, counts)
+        except ValueError as err:
+            meta = str(err)
+    box = [meta]
+    dist.broadcast_object_list(box, src=root, group=self.group)
+    if isinstance(box[0], str):
+        raise ValueError(box[0])
+    n, counts = box[0][0], box[0][1:]
+    if out is None:
+        out = torch.empty(counts[me], dtype=torch.float32, device=self.device)
+    lib = L.lib()
+    s = self.stream.cuda_stream
+    if N == 1:
+        out.copy_(x)
+        self.launches_per_call = 1
+        return out
+    order = [(root + j) % N for j in range(N)]  # virtual rank -> actual rank
+    vcounts = [counts[order[v]] for v in range(N)]
+    key = (n, tuple(counts), root, routing)
+    if getattr(self, "_sc_key", None) != key:
+        _scatter_close(self)
+        self._sc_layout = _ScatterLayout(N, vcounts)
+        self._sc_buf = torch.zeros(self._sc_layout.total, dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        self._sc_peer = _open_peers(self, self._sc_buf)
+        self._sc_key = key
+        self._sc_epoch = 0
+        dist.barrier(group=self.group)
+    lay, peer = self._sc_layout, self._sc_peer
+    prev, e = self._sc_epoch, self._sc_epoch + 1
+    vr = (me - root) % N
+    parent, _, sends = scatter_route(N, root)[me]
+    launches = 0
+
+    def at(r, off):
+        return peer[r] + off
+
+    if me == root:
+        # blobs of the previous call must be consumed before they are overwritten
+        if prev:
+            for j in ([c for c, _, _ in sends] if routing == "tree" else [j for j in range(N) if j != me]):
+                L.check(lib.gz_stream_wait_u32_geq(s, at(me, lay.consumed(j)), prev), "gz_stream_wait_u32_geq")
+        lo = [0]
+        for c in counts:
+            lo.append(lo[-1] + c)
+        xv = x if root == 0 else torch.cat([x[lo[r]:lo[r + 1]] for r in order])
+        arr = ctypes.c_uint64 * N
+        h_counts = arr(*vcounts)
+        ws = self.ws.tile_ws(int(lib.gz_segments_workspace_bytes(h_counts, N)))
+        base = self._sc_buf.data_ptr()
+        L.check(lib.gz_compress_segments(xv.data_ptr(), h_counts, N, ebf, base, arr(*lay.slot), base + lay.len_off,
+                                         base, arr(*lay.sc), ws.data_ptr(), ws.numel(), self.ws.status_ptr(), s),
+                "gz_compress_segments")
+        out.copy_(x[lo[me]:lo[me + 1]])
+        launches += 2 + (root != 0)
+        targets = [c for c, _, _ in sends] if routing == "tree" else [j for j in range(N) if j != me]
+        for j in targets:
+            L.check(lib.gz_stream_write_u32(s, at(j, lay.READY), e), "gz_stream_write_u32")
+    else:
+        L.check(lib.gz_stream_wait_u32_geq(s, at(me, lay.READY), e), "gz_stream_wait_u32_geq")
+        if routing == "tree":
+            # my children must be done with my previous range before I overwrite it
+            if prev:
+                for c, _, _ in sends:
+                    L.check(lib.gz_stream_wait_u32_geq(s, at(me, lay.consumed(c)), prev), "gz_stream_wait_u32_geq")
+            hi = max([h for _, _, h in sends], default=vr + 1)
+            items = [_CopyItem(at(parent, lay.len_off + 8 * vr), at(me, lay.len_off + 8 * vr), None, 8 * (hi - vr))]
+            for v in range(vr, hi):
+                items.append(_CopyItem(at(parent, lay.slot[v]), at(me, lay.slot[v]), at(parent, lay.len_off + 8 * v),
+                                       lay.cap[v]))
+                items.append(_CopyItem(at(parent, lay.sc[v]), at(me, lay.sc[v]), None, lay.sc_bytes[v]))
+            for k in range(0, len(items), 64):
+                chunk = items[k:k + 64]
+                L.check(lib.gz_copy_items((_CopyItem * len(chunk))(*chunk), len(chunk), s), "gz_copy_items")
+                launches += 1
+            # parent's range has been read: release it, then wake my children
+            L.check(lib.gz_stream_write_u32(s, at(parent, lay.consumed(me)), e), "gz_stream_write_u32")
+            for c, _, _ in sends:
+                L.check(lib.gz_stream_write_u32(s, at(c, lay.READY), e), "gz_stream_write_u32")
+            src = me
+        else:
+            src = root
+        L.check(lib.gz_decompress_sidecar(at(src, lay.slot[vr]), at(src, lay.sc[vr]), counts[me], ebf, out.data_ptr(),
+                                          self.ws.status_ptr(), s), "gz_decompress_sidecar")
+        launches += 1
+        if routing == "direct":
+            L.check(lib.gz_stream_write_u32(s, at(root, lay.consumed(me)), e), "gz_stream_write_u32")
+    self._sc_epoch = e
+    self.launches_per_call = launches
+    return out
+
+
+Communicator.binomial_scatter = binomial_scatter

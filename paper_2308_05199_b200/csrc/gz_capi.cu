@@ -125,8 +125,38 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   }
   a.nctas = base;
   a.total_tiles = total_tiles;
+  // tiles per gather CTA: 32, doubled until the grid fits MAXGRID
+  uint32_t gt = GATHER_MIN_TILES;
+  uint64_t gbase = 0;
+  while (true) {
+    gbase = 0;
+    for (int k = 0; k < a.nseg; ++k) gbase += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + gt - 1) / gt);
+    if (gbase <= (uint64_t)MAXGRID || gt >= (uint32_t)GATHER_THREADS) break;
+    gt *= 2;
+  }
+  if (gbase > (uint64_t)MAXGRID) return GZ_EINVAL;
+  gbase = 0;
+  for (int k = 0; k < a.nseg; ++k) {
+    a.seg[k].gcta_base = gbase;
+    gbase += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + gt - 1) / gt);
+  }
+  a.gtiles = gt;
+  a.ngctas = gbase;
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
-  return (int)cudaGetLastError();
+  int rc = (int)cudaGetLastError();
+  if (rc) return rc;
+  // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)gbase);
+  cfg.blockDim = dim3(GATHER_THREADS);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, k_gather<NSEG>, a);
 }
 
 template <int SRC, int NSEG>
@@ -142,6 +172,28 @@ __global__ void k_copy_blob(const uint4* __restrict__ src, uint4* __restrict__ d
   const uint64_t nch = (len + 15) >> 4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nch; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = __ldcs(src + i);
+}
+
+struct CopyItems {
+  gz_copy_item it[GZ_MAX_COPY_ITEMS];
+};
+
+// blockIdx.y = item; 16-byte body, byte tail.
+__global__ void k_copy_items(const CopyItems ci) {
+  const gz_copy_item& it = ci.it[blockIdx.y];
+  const uint64_t len = it.d_len ? umin64(*it.d_len, it.max_bytes) : it.max_bytes;
+  if (((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15) != 0) {
+    // unaligned (small) item: byte copy
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x)
+      it.dst[i] = it.src[i];
+    return;
+  }
+  const uint64_t nch = len >> 4;
+  const uint4* s = reinterpret_cast<const uint4*>(it.src);
+  uint4* d = reinterpret_cast<uint4*>(it.dst);
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nch; i += (uint64_t)gridDim.x * blockDim.x)
+    d[i] = __ldcs(s + i);
+  if (blockIdx.x == 0 && threadIdx.x < (len & 15)) it.dst[(nch << 4) + threadIdx.x] = it.src[(nch << 4) + threadIdx.x];
 }
 
 struct IpcHandle {
@@ -218,7 +270,7 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0};
+  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
@@ -322,7 +374,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView so = sidecar_view(sidecar_out, m);
-  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0};
+  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   const WsView wv = carve(ws, ntiles_of(m));
@@ -373,7 +425,7 @@ int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg
       const uint64_t n = h_counts[i];
       SidecarView sv{nullptr, nullptr};
       if (sidecars) sv = sidecar_view(reinterpret_cast<uint8_t*>(sidecars) + h_seg_sidecar_off[i], n);
-      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, tiles};
+      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, 0, tiles};
       tiles += ntiles_of(n);
       xoff += n;
     }
@@ -455,6 +507,23 @@ int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64
   if (!src || !dst || !d_len || !aligned16(src) || !aligned16(dst)) return GZ_EINVAL;
   k_copy_blob<<<296, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
                                                       d_len, max_bytes);
+  return (int)cudaGetLastError();
+}
+
+int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream) {
+  if (count == 0) return 0;
+  if (!items || count > GZ_MAX_COPY_ITEMS) return GZ_EINVAL;
+  CopyItems ci;
+  memset(&ci, 0, sizeof(ci));
+  for (uint32_t i = 0; i < count; ++i) {
+    if (!items[i].src || !items[i].dst) return GZ_EINVAL;
+    ci.it[i] = items[i];
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const unsigned gx = (unsigned)std::max(1, 2 * sms / (int)count);
+  k_copy_items<<<dim3(gx, count), 256, 0, (cudaStream_t)stream>>>(ci);
   return (int)cudaGetLastError();
 }
 

@@ -24,7 +24,8 @@ struct Seg {
   uint64_t* out_len;       // 24 + payload bytes
   uint64_t* out_tile_off;  // sidecar: [ntiles + 1] payload offsets of tiles
   uint16_t* out_sub_off;   // sidecar: [ntiles * GROUPS] offsets of every 8th block inside its tile
-  uint64_t cta_base;       // first CTA (ticket) of this segment
+  uint64_t cta_base;       // first encoder CTA of this segment
+  uint64_t gcta_base;      // first gather CTA (ticket) of this segment
   uint64_t tile_base;      // first slot of this segment in tile_rel / scratch
 };
 
@@ -32,8 +33,10 @@ template <int NSEG>
 struct EncodeArgs {
   Seg seg[NSEG];
   int nseg;
-  uint64_t nctas;          // CTAs (== grid), split over segments by cta_base
-  uint64_t total_tiles;    // tiles over all segments (phase A tickets)
+  uint64_t nctas;          // encoder CTAs (== grid), split over segments by cta_base
+  uint64_t ngctas;         // gather CTAs, `gtiles` tiles each, split by gcta_base
+  uint32_t gtiles;         // tiles per gather CTA (32..GATHER_THREADS)
+  uint64_t total_tiles;    // tiles over all segments
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
   TileWs* ws;
@@ -461,19 +464,6 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   const int nval = (int)(G.n - v0 < (uint64_t)TILE_VALUES ? G.n - v0 : (uint64_t)TILE_VALUES);
   int base = 0;
 
-  if (tile == 0 && lane < 6) {  // codec.py:158, HEADER "<4s4xQd"
-    uint32_t hw;
-    if (lane == 0) hw = 0x31435A47u;  // "GZC1"
-    else if (lane == 1) hw = 0;
-    else if (lane == 2) hw = (uint32_t)G.n;
-    else if (lane == 3) hw = (uint32_t)(G.n >> 32);
-    else {
-      const unsigned long long eb = __double_as_longlong(a.qp.eb);
-      hw = lane == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
-    }
-    reinterpret_cast<uint32_t*>(S.blob)[lane] = hw;
-  }
-
   // ---- 1. fused step: combine the received blob's tile into xs
   if (SRC == SRC_STEP) {
     const uint64_t ts = a.in_tile_off[tile], te = a.in_tile_off[tile + 1];
@@ -749,51 +739,39 @@ __device__ __forceinline__ void warp_copy4(uint8_t* const (&dst)[4], const uint8
   }
 }
 
-// Encoder (one launch, one CTA per SM, no grid-wide barrier).
-//   A. CTA c owns a contiguous tile range of one segment (CTAs are split over
-//      segments in proportion to their tiles; c is an atomic ticket, so a CTA
-//      only ever waits for CTAs that are running).  Its warps claim tiles of
-//      the range from a shared-memory counter -- warps of one SM do not get
-//      equal issue slots, so the work must be balanced dynamically -- and
-//      prefetch the next claimed tile (cp.async, L2 evict_first) while they
-//      quantise the current one.  Each tile is packed into its own aligned
-//      scratch slot (L2 evict_last).
-//   B. The CTA publishes its byte total and sums the totals of the segment's
-//      earlier CTAs (the exclusive scan of codec.py:241-243 as a decoupled
-//      prefix), scans its tiles' sizes, and copies every slot to its final
-//      offset -- possibly in a peer GPU's memory (the NVLink send of a fused
-//      reduce-scatter step) -- one lane per tile, then drops the slots from L2.
+// Encoder, kernel 1 of 2 (one CTA per SM, no CTA-wide barrier after setup).
+// CTA c owns a contiguous tile range of one segment (CTAs are split over
+// segments in proportion to their tiles).  Its warps claim tiles of the range
+// from a shared-memory counter -- warps of one SM do not get equal issue
+// slots, so the work is balanced dynamically -- and prefetch the next claimed
+// tile (cp.async, L2 evict_first) while they quantise the current one.  Each
+// tile is packed into its own 128-byte aligned scratch slot (L2 evict_last)
+// and its size recorded; a warp with no tile left simply exits.  The
+// position-independent parts of the sidecar (sub-offsets) are final here.
 template <int SRC, int NSEG, bool FAST>
 __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const EncodeArgs<NSEG> a) {
   constexpr int NW = enc_warps(SRC);
-  constexpr int NT = 32 * NW;
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
   __shared__ uint16_t s_start[SRC == SRC_STEP ? NW : 1][TB];
   __shared__ uint8_t s_w[SRC == SRC_STEP ? NW : 1][TB];
-  __shared__ unsigned long long s_cta, s_gen, s_base, s_carry;
   __shared__ unsigned int s_next;
-  __shared__ unsigned long long s_red[NW];
-  __shared__ unsigned long long s_off[NT];
-  __shared__ uint32_t s_sz[NT];
+  // the gather kernel may be scheduled as soon as SMs free up; it waits for
+  // this grid's completion itself (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int WSMEM = SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4;
   unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
   float* xsb1 = reinterpret_cast<float*>(my + TILE_VALUES * 4);
   uint32_t* stage = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);  // fused step only
-  TileWs* ws = a.ws;
   const int wi = SRC == SRC_STEP ? warp : 0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
-  if (tid == 0) {
-    s_cta = atomicAdd(&ws->ticket, 1ull);
-    s_gen = ld_volatile_u64(&ws->gen);
-    s_next = 0;
-  }
+  if (tid == 0) s_next = 0;
   __syncthreads();
-  const unsigned long long c = s_cta, gen = s_gen;
+  const uint64_t c = blockIdx.x;
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
-  const unsigned long long ts0 = gtimer();
+  const unsigned long long ts0 = a.dbg ? gtimer() : 0;
 
   // ---- this CTA's segment and tile range
   int k = 0;
@@ -811,7 +789,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   uint32_t* const sizes = a.tile_rel + S.tile_base;
   uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
 
-  // ---- phase A: warps claim tiles of [r0, r1) dynamically
   auto claim = [&]() -> unsigned int {
     unsigned int v = 0;
     if (lane == 0) v = atomicAdd(&s_next, 1u);
@@ -833,7 +810,10 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
                                                 reinterpret_cast<uint32_t*>(slots + t * (uint64_t)TILE_SLOT), 0, false,
                                                 dummy, stage, s_start[wi], s_w[wi], s_step, pol_keep, lane);
-    if (lane == 0) sizes[t] = (uint32_t)tb;
+    if (lane == 0) {
+      sizes[t] = (uint32_t)tb;
+      atomicAdd(&a.ws->agg[S.gcta_base + t / a.gtiles], (unsigned)tb);
+    }
     ++ndone;
     __syncwarp();
     buf ^= 1;
@@ -841,136 +821,204 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     j1 = j < nr ? claim() : nr;
   }
   cp_async_wait_all();
-  const unsigned long long ts1 = gtimer();
-  __syncthreads();  // every tile of the range is in its slot, sizes written
-
-  // ---- phase B: CTA total, decoupled prefix over earlier CTAs
-  unsigned long long tot = 0;
-  for (unsigned int q = tid; q < nr; q += NT) tot += sizes[r0 + q];
-  tot = warp_sum_u64(tot);
-  if (lane == 0) s_red[warp] = tot;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long t2 = 0;
-#pragma unroll
-    for (int q = 0; q < NW; ++q) t2 += s_red[q];
-    s_carry = t2;
-    st_volatile_u64(&ws->status[c], mk_status(gen, 1u, t2));
-  }
-  unsigned long long part = 0;
-  for (uint64_t p = cta_lo + tid; p < c; p += NT) {
-    unsigned long long sw;
-    while (true) {
-      sw = ld_volatile_u64(&ws->status[p]);
-      if (((sw >> 48) & 0xFFFF) == (gen & 0xFFFF) && ((sw >> 46) & 3) != 0) break;
-      __nanosleep(32);
-    }
-    part += sw & VALUE_MASK;
-  }
-  __syncthreads();  // s_red reuse
-  part = warp_sum_u64(part);
-  if (lane == 0) s_red[warp] = part;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long b = 0;
-#pragma unroll
-    for (int q = 0; q < NW; ++q) b += s_red[q];
-    s_base = b;
-  }
-  __syncthreads();
-  const unsigned long long ts2 = gtimer();
-
-  // ---- phase B: block-wide scan of the range's tile sizes; each warp copies
-  // the 32 tiles its lanes own, four at a time (coalesced, loads batched)
-  unsigned long long run = s_base;
-  for (unsigned int q0 = 0; q0 < nr; q0 += NT) {
-    const unsigned int q = q0 + tid;
-    const unsigned long long sz = q < nr ? sizes[r0 + q] : 0ull;
-    unsigned long long incl = sz;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const unsigned long long v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-      if (lane >= d) incl += v;
-    }
-    __syncthreads();
-    if (lane == 31) s_red[warp] = incl;
-    __syncthreads();
-    unsigned long long wpre = 0, rtot = 0;
-#pragma unroll
-    for (int w2 = 0; w2 < NW; ++w2) {
-      wpre += w2 < warp ? s_red[w2] : 0ull;
-      rtot += s_red[w2];
-    }
-    const unsigned long long o = run + wpre + incl - sz;
-    if (q < nr) {
-      const uint64_t t = r0 + q;
-      if (S.out_tile_off) S.out_tile_off[t] = o;
-      if (a.blk_off && k == 0) {
-        const uint64_t bb0 = t * TB, bb1 = umin64(bb0 + TB, G.nb);
-        for (uint64_t b = bb0; b < bb1; ++b) a.blk_off[b] += o;
-      }
-    }
-    if (q < nr) {
-      s_off[tid] = o;
-      s_sz[tid] = (uint32_t)sz;
-    }
-    __syncthreads();
-    // tiles of this round are spread over all warps: warp w copies w, w+NW, ...
-    const unsigned int cnt = (unsigned int)min((unsigned long long)NT, (unsigned long long)(nr - q0));
-    for (unsigned int r = warp; r < cnt; r += 4 * NW) {
-      uint8_t* dsts[4];
-      const uint8_t* srcs[4];
-      int lens[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const unsigned int rr = r + i * NW;
-        const bool v = rr < cnt;
-        const unsigned int rc = v ? rr : r;
-        dsts[i] = S.blob + HEADER_BYTES + s_off[rc];
-        srcs[i] = slots + (r0 + q0 + rc) * (uint64_t)TILE_SLOT;
-        lens[i] = v ? (int)s_sz[rc] : 0;
-      }
-      warp_copy4(dsts, srcs, lens, lane);
-    }
-    __syncthreads();
-    run += rtot;
-  }
-  const unsigned long long tb3 = gtimer();
-  // the segment's last CTA knows the total: blob length and end offset
-  if (c == cta_hi - 1 && tid == 0) {
-    const unsigned long long total = s_base + s_carry;
-    if (S.out_tile_off) S.out_tile_off[G.ntiles] = total;
-    *S.out_len = HEADER_BYTES + total;
-    if (G.ntiles == 0) {  // empty blob: header only (codec.py:159-160)
-      uint32_t* hb = reinterpret_cast<uint32_t*>(S.blob);
-      const unsigned long long eb = __double_as_longlong(a.qp.eb);
-      hb[0] = 0x31435A47u;
-      hb[1] = 0;
-      hb[2] = 0;
-      hb[3] = 0;
-      hb[4] = (uint32_t)eb;
-      hb[5] = (uint32_t)(eb >> 32);
-    }
-  }
   if (a.dbg && lane == 0) {  // experiments: per-warp timestamps
     unsigned long long* d = a.dbg + (c * NW + warp) * 12;
-    d[0] = ts0; d[1] = ts1; d[2] = ts2; d[3] = gtimer(); d[4] = ndone;
-    d[5] = wait_ns; d[6] = c; d[7] = tb3; d[8] = tb3; d[9] = tb3;
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    d[10] = smid;
-    d[11] = ndone;
+    d[0] = ts0; d[1] = gtimer(); d[2] = ndone; d[3] = wait_ns; d[4] = c; d[5] = smid;
   }
-  // retire: the last CTA resets the ticket and bumps gen
+}
+
+// Encoder, kernel 2 of 2: the exclusive scan of codec.py:241-243 at tile
+// granularity and the gather of the slots into the blob.  Gather CTA g of a
+// segment owns `gtiles` consecutive tiles.  The encoder has added every
+// tile's size into agg[g], so the CTA's base offset is a plain parallel sum
+// of the segment's earlier agg[] entries (no look-back, no waiting); a block
+// scan of its tiles' sizes gives the tile offsets, and every thread then
+// produces aligned 16-byte chunks of the CTA's contiguous output range --
+// possibly in a peer GPU's memory (the NVLink send of a fused
+// reduce-scatter step) -- coalesced.  Launched as a programmatic dependent
+// of the encoder, so its launch overlaps the encoder's tail.
+constexpr int GATHER_THREADS = 128;
+constexpr int GATHER_MIN_TILES = 32;
+
+// 16 bytes from any byte address inside a slot (two aligned loads + funnel)
+__device__ __forceinline__ uint4 ld16u(const uint8_t* src) {
+  const uint4* s4 = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15);
+  const int h = (int)(reinterpret_cast<uintptr_t>(src) & 15), wo = h >> 2, sh = (h & 3) * 8;
+  const uint4 cur = __ldcs(s4);
+  const uint4 nxt = h ? __ldcs(s4 + 1) : cur;
+  const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+  const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+  const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+  const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+  const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+  return make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh), __funnelshift_r(a2, a3, sh),
+                    __funnelshift_r(a3, a4, sh));
+}
+
+// 16 bytes of the CTA's output starting at local byte p, which lies in tile
+// i: one unaligned read out of tile i's slot, merged with the start of tile
+// i+1 when the chunk crosses the boundary (tiles other than a segment's last
+// are >= 160 bytes, so a chunk never spans three tiles).
+__device__ __forceinline__ uint4 gather16(const uint8_t* slots0, const uint32_t* loc, int i, uint32_t p) {
+  const uint4 A = ld16u(slots0 + (uint64_t)i * TILE_SLOT + (p - loc[i]));
+  const uint32_t k = loc[i + 1] - p;  // bytes of the chunk inside tile i
+  if (k >= 16) return A;
+  const uint4 B = ld16u(slots0 + (uint64_t)(i + 1) * TILE_SLOT);
+  // out byte b = b < k ? A[b] : B[b - k]
+  const uint32_t a[4] = {A.x, A.y, A.z, A.w}, bw[4] = {B.x, B.y, B.z, B.w};
+  const int ws = (int)(k >> 2), sh = (int)(k & 3) * 8;
+  uint32_t o[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int q = j - ws;
+    const uint32_t hi = q >= 0 ? bw[q] : 0u, lo = q >= 1 ? bw[q - 1] : 0u;
+    const uint32_t bsh = __funnelshift_l(lo, hi, sh);  // B shifted up by k bytes
+    const int nb = (int)k - 4 * j;                     // bytes of word j taken from A
+    const uint32_t m = nb >= 4 ? 0xFFFFFFFFu : nb <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * nb));
+    o[j] = (a[j] & m) | (bsh & ~m);
+  }
+  return make_uint4(o[0], o[1], o[2], o[3]);
+}
+
+template <int NSEG>
+__global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG> a) {
+  constexpr int NWG = GATHER_THREADS / 32;
+  __shared__ uint32_t s_wsum[NWG];
+  __shared__ unsigned long long s_red[NWG];
+  __shared__ uint32_t s_loc[GATHER_THREADS + 1];  // local payload offset of each tile, [nr] = total
+  __shared__ int s_last;
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // the encoder grid is complete
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  TileWs* ws = a.ws;
+  const uint64_t c = blockIdx.x;
+  int k = 0;
+  if (NSEG > 1) {
+#pragma unroll 1
+    for (int i = 1; i < a.nseg; ++i)
+      if (a.seg[i].gcta_base <= c) k = i;
+  }
+  const Seg& S = a.seg[k];
+  const uint64_t glo = S.gcta_base, ghi = (k + 1 < a.nseg) ? a.seg[k + 1].gcta_base : a.ngctas;
+  const SegGeom G = seg_geom(S.n);
+  const uint64_t r0 = (c - glo) * a.gtiles;
+  const uint64_t r1 = umin64(r0 + a.gtiles, G.ntiles);
+  const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
+  const uint32_t* const sizes = a.tile_rel + S.tile_base;
+  const uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
+
+  // ---- base offset: bytes of the segment's earlier gather CTAs
+  unsigned long long part = 0;
+  for (uint64_t g = glo + tid; g < c; g += GATHER_THREADS) part += ws->agg[g];
+  part = warp_sum_u64(part);
+  // ---- block scan of this CTA's tile sizes
+  const uint32_t sz = tid < nr ? sizes[r0 + tid] : 0u;
+  uint32_t incl = sz;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  if (lane == 0) s_red[warp] = part;
+  __syncthreads();
+  uint32_t wpre = 0, agg = 0;
+  unsigned long long excl = 0;
+#pragma unroll
+  for (int w2 = 0; w2 < NWG; ++w2) {
+    wpre += w2 < warp ? s_wsum[w2] : 0u;
+    agg += s_wsum[w2];
+    excl += s_red[w2];
+  }
+  if (tid < nr) {
+    const uint64_t t = r0 + tid;
+    const unsigned long long o = excl + wpre + incl - sz;
+    if (S.out_tile_off) S.out_tile_off[t] = o;
+    if (a.blk_off && k == 0) {
+      const uint64_t bb0 = t * TB, bb1 = umin64(bb0 + TB, G.nb);
+      for (uint64_t b = bb0; b < bb1; ++b) a.blk_off[b] += o;
+    }
+    s_loc[tid] = wpre + incl - sz;
+  }
+  if (tid == 0) s_loc[nr] = agg;
+  if (c == glo && tid < 6) {  // codec.py:158, HEADER "<4s4xQd"
+    uint32_t hw;
+    if (tid == 0) hw = 0x31435A47u;  // "GZC1"
+    else if (tid == 1) hw = 0;
+    else if (tid == 2) hw = (uint32_t)G.n;
+    else if (tid == 3) hw = (uint32_t)(G.n >> 32);
+    else {
+      const unsigned long long eb = __double_as_longlong(a.qp.eb);
+      hw = tid == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
+    }
+    reinterpret_cast<uint32_t*>(S.blob)[tid] = hw;
+  }
+  if (c == ghi - 1 && tid == 0) {  // the segment's last CTA knows the total
+    const unsigned long long total = excl + agg;
+    if (S.out_tile_off) S.out_tile_off[G.ntiles] = total;
+    *S.out_len = HEADER_BYTES + total;
+  }
+  __syncthreads();
+  // ---- copy: aligned 16-byte destination chunks; the source tile of a
+  // chunk by binary search over the local offsets; ragged ends byte-wise
+  // (they share a chunk with the neighbouring CTAs' ranges)
+  {
+    uint8_t* const base = S.blob + HEADER_BYTES + excl;
+    const uint8_t* const sl0 = slots + r0 * (uint64_t)TILE_SLOT;
+    const uintptr_t A = reinterpret_cast<uintptr_t>(base), E = A + agg;
+    const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cle = E & ~(uintptr_t)15;
+    auto find = [&](uint32_t p) {
+      int lo = 0, hi = nr - 1;  // last i with s_loc[i] <= p
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_loc[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      return lo;
+    };
+    auto byte_at = [&](uint32_t p) {
+      const int i = find(p);
+      return sl0[(uint64_t)i * TILE_SLOT + (p - s_loc[i])];
+    };
+    if (cf < cle) {
+      const uint32_t head = (uint32_t)(cf - A);
+      const uint32_t nch = (uint32_t)((cle - cf) >> 4);
+      uint4* d4 = reinterpret_cast<uint4*>(cf);
+      constexpr int B = 4;
+      for (uint32_t c0 = tid; c0 < nch; c0 += B * GATHER_THREADS) {
+        uint4 v[B];
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+          const uint32_t ch = c0 + m * GATHER_THREADS;
+          if (ch < nch) {
+            const uint32_t p = head + 16 * ch;
+            v[m] = gather16(sl0, s_loc, find(p), p);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < B; ++m) {
+          const uint32_t ch = c0 + m * GATHER_THREADS;
+          if (ch < nch) d4[ch] = v[m];
+        }
+      }
+      const uint32_t tail0 = head + 16 * nch;
+      if (tid < head) base[tid] = byte_at(tid);
+      if (tid >= 32 && tid - 32 < agg - tail0) base[tail0 + (tid - 32)] = byte_at(tail0 + (tid - 32));
+    } else {
+      for (uint32_t p = tid; p < agg; p += GATHER_THREADS) base[p] = byte_at(p);
+    }
+  }
+  // ---- retire: the last CTA zeroes agg[] for the next launch
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    if (atomicAdd(&ws->done, 1ull) == a.nctas - 1) {
-      ws->done = 0;
-      ws->ticket = 0;
-      __threadfence();
-      atomicAdd(&ws->gen, 1ull);
-    }
+    s_last = atomicAdd(&ws->done, 1ull) == a.ngctas - 1;
+  }
+  __syncthreads();
+  if (s_last) {
+    for (uint64_t g = tid; g < a.ngctas; g += GATHER_THREADS) ws->agg[g] = 0;
+    if (tid == 0) ws->done = 0;
   }
 }
 

@@ -48,19 +48,16 @@ constexpr float MAGIC32 = 12582912.0f;                     // 1.5 * 2^23
 constexpr int MAGIC32_BITS = 0x4B400000;
 
 // ---- device workspace: zero-initialised once, reused by every launch -------
-// Layout: this header, status[MAXGRID], tile_rel[ntiles] (u32), scratch.
-// status[c] = gen(16) | flag(2) | value(46): flag 1 = CTA aggregate.  `gen`
-// advances when the last CTA of a launch retires, so no per-launch memset is
-// needed and CUDA-graph replay is safe.
-constexpr int MAXGRID = 4096;
+// Layout: this header, tile sizes (u32 per tile), scratch slots.
+// agg[g] = compressed bytes of gather CTA g's tiles, accumulated by the
+// encoder kernel and zeroed again by the last gather CTA to retire, so no
+// per-launch memset is needed and CUDA-graph replay is safe.
+constexpr int MAXGRID = 16384;   // gather CTAs per launch
 constexpr int TILE_SLOT = 4224;  // scratch bytes reserved per tile (>= 32 * 129, 128-aligned)
 struct TileWs {
-  unsigned long long ticket;        // dynamic tile tickets (own 128-byte line)
+  unsigned long long done;          // gather retire counter (own 128-byte line)
   unsigned long long pad0[15];
-  unsigned long long done;          // retire counter (own line)
-  unsigned long long gen;
-  unsigned long long pad1[14];
-  unsigned long long status[MAXGRID];
+  unsigned int agg[MAXGRID];
 };
 
 struct Status {                          // error reporting (host-reset to ~0)
@@ -331,9 +328,4 @@ __device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned lon
 __device__ __forceinline__ void st_volatile_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
-constexpr unsigned long long VALUE_MASK = (1ull << 46) - 1;
-__device__ __forceinline__ unsigned long long mk_status(unsigned long long gen, unsigned flag, unsigned long long v) {
-  return ((gen & 0xFFFF) << 48) | ((unsigned long long)flag << 46) | (v & VALUE_MASK);
-}
-
 }  // namespace gz

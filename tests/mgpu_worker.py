@@ -55,6 +55,41 @@ def main():
         if out.cpu().numpy().tobytes() != expect[rank].tobytes():
             failures.append(f"oracle n={n} op={op} eb={eb}")
         checked += 1
+    # binomial scatter: golden cases of this rank count, then seeded cases at every root
+    for case in G.scatter_cases():
+        if case.N != world:
+            continue
+        for routing in ("tree", "direct"):
+            for rep in range(2):
+                x = torch.from_numpy(np.ascontiguousarray(case.data, np.float32)).to(dev) if rank == case.root else None
+                out = c.binomial_scatter(x, 1e-4, counts=case.counts, root=case.root, routing=routing)
+                torch.cuda.synchronize()
+                if out.cpu().numpy().tobytes() != case.outputs[rank].tobytes():
+                    failures.append(f"scatter golden root={case.root} counts={case.counts} {routing} rep={rep}")
+                checked += 1
+    for n, eb, counts in ((1 << 22, 1e-4, None), (1_000_003, 1e-3, None),
+                          (9_999, 1e-4, [0] * (world - 1) + [9_999]),
+                          (5_000_000, 1e-5, [5_000_000 // world + (7 if r % 2 else -7) for r in range(world)])):
+        data = O.smooth_field(n, 0.11) + np.random.default_rng(n).normal(0, 1e-3, n).astype(np.float32)
+        if counts is not None and sum(counts) != n:
+            counts[-1] += n - sum(counts)
+        for root in range(world):
+            expect = O.binomial_scatter(data, world, eb, root=root, counts=counts)
+            for routing in ("tree", "direct"):
+                x = torch.from_numpy(data).to(dev) if rank == root else None
+                out = c.binomial_scatter(x, eb, counts=counts, root=root, routing=routing)
+                torch.cuda.synchronize()
+                if out.cpu().numpy().tobytes() != expect[rank].tobytes():
+                    failures.append(f"scatter oracle n={n} eb={eb} root={root} {routing}")
+                checked += 1
+    # bad counts: every rank raises the root's error
+    try:
+        c.binomial_scatter(torch.zeros(10, device=dev) if rank == 0 else None, 1e-4, counts=[1] * world, root=0)
+        failures.append("bad counts accepted")
+    except ValueError as err:
+        if "sum" not in str(err):
+            failures.append(f"bad counts message {err}")
+    checked += 1
     flag = torch.tensor([len(failures)], device=dev)
     dist.all_reduce(flag)
     if rank == 0:
