@@ -208,6 +208,7 @@ def bench_codec(args):
         dec()
     torch.cuda.synchronize()
     tc, td = [], []
+    launches0 = int(lib.gz_launch_count())
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         for _ in range(args.steps):
@@ -222,6 +223,7 @@ def bench_codec(args):
             tc.append(e0.elapsed_time(e1) * 1e-3)
             td.append(e1.elapsed_time(e2) * 1e-3)
     torch.cuda.synchronize()
+    launches = int(lib.gz_launch_count()) - launches0
     # parity of the timed output against the oracle-pinned first blob
     assert bytes(out[:Lb].cpu().numpy().tobytes()) == bytes(blob0), "timed blob differs"
     t_c, t_d = sum(tc) / len(tc), sum(td) / len(td)
@@ -269,7 +271,7 @@ def bench_codec(args):
                    "l2": "flushed (256 MB write) before every timed step",
                    "compress_us": round(t_c * 1e6, 2), "decompress_us": round(t_d * 1e6, 2),
                    "compress_hbm_gbs": round(achieved_c, 1), "decompress_hbm_gbs": round(bytes_d / t_d / 1e9, 1)},
-        "roofline": {"bound": "hbm", "kernel": "k_tile_encode (compress)", "achieved": round(achieved_c, 1),
+        "roofline": {"bound": "hbm", "kernel": "compress = k_tile_encode + k_gather", "achieved": round(achieved_c, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved_c / peak, 4),
                      "traffic": traffic, "algorithmic_bytes_per_launch": bytes_c},
         "cpu_baseline": {"value": round(cpu_gbs, 4), "unit": "GB/s", "cores": thr, "kind": "port",
@@ -277,7 +279,7 @@ def bench_codec(args):
         "e2e": {"value": round(e2e, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n + Lb, "d2h_bytes_per_step": Lb + 4 * n,
                 "api": "compress(pinned host f32 tensor) -> pinned host blob; decompress(host blob) -> pinned host f32",
                 "wall_ms_per_step": round(sum(e2e_t) / len(e2e_t) * 1e3, 3)},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": launches,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
@@ -289,10 +291,20 @@ def bench_codec(args):
 # ---------------------------------------------------------------------------
 
 
+def _max_over_ranks(v: float, dev) -> float:
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def bench_allreduce(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2308_05199_b200 import _lib as L
     from paper_2308_05199_b200 import comm
     from oracle import oracle as O
 
@@ -302,53 +314,120 @@ def bench_allreduce(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    n = S_CFG1_elems = S_CFG2 // 4
+    lib = L.lib()
+    n = S_CFG2 // 4
     xh = O.smooth_field(n, 0.37 * rank)
     x = torch.from_numpy(xh).to(dev)
     c = comm.Communicator(dist.group.WORLD, dev)
     out = torch.empty_like(x)
     stream = torch.cuda.current_stream()
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
     for _ in range(max(args.warmup, 3)):
         c.ring_allreduce(x, EB, out=out)
     torch.cuda.synchronize()
     dist.barrier()
-    times = []
+    times, step_t = [], []
+    launches0 = int(lib.gz_launch_count())
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             dist.barrier()
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c.events = []  # marks after every wait/launch: fused-step kernel durations
+            e0, e1 = ev(), ev()
             e0.record(stream)
             c.ring_allreduce(x, EB, out=out)
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) * 1e-3)
-    t_local = sum(times) / len(times)
-    tt = torch.tensor([t_local], device=dev, dtype=torch.float64)
-    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-    t = float(tt.item())
-    # NCCL comparator on the same tensor
+            marks = c.events
+            for (_, a), (lab, b) in zip(marks, marks[1:]):
+                if lab in ("reduce", "reduce_last"):
+                    step_t.append(a.elapsed_time(b) * 1e-3)
+            c.events = None
+    launches = int(lib.gz_launch_count()) - launches0
+    t = _max_over_ranks(sum(times) / len(times), dev)
+    cr = c.compression_ratio()
+    m = n // world
+    t_step = sum(step_t) / len(step_t)
+    step_bytes = 4 * m + 2 * 4 * m / (cr or 1.0)  # local chunk + received blob + produced blob
+    step_gbs = _max_over_ranks(-step_bytes / t_step / 1e9, dev) * -1.0  # slowest rank
+
+    # e2e: pinned host input -> H2D -> allreduce -> D2H of the result, per step
+    xp = torch.from_numpy(xh).pin_memory()
+    outp = torch.empty(n, dtype=torch.float32).pin_memory()
+    e2e_t = []
+    for i in range(max(3, min(args.steps, 5)) + 1):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        x.copy_(xp, non_blocking=True)
+        c.ring_allreduce(x, EB, out=out)
+        outp.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i:
+            e2e_t.append(e0.elapsed_time(e1) * 1e-3)
+    t_e2e = _max_over_ranks(sum(e2e_t) / len(e2e_t), dev)
+
+    # NCCL all_reduce comparator on the same tensor
     y = x.clone()
     for _ in range(3):
         dist.all_reduce(y)
     torch.cuda.synchronize()
-    dist.barrier()
     nt = []
     for _ in range(max(3, min(args.steps, 10))):
         y.copy_(x)
         dist.barrier()
         torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0, e1 = ev(), ev()
         e0.record(stream)
         dist.all_reduce(y)
         e1.record(stream)
         torch.cuda.synchronize()
         nt.append(e0.elapsed_time(e1) * 1e-3)
-    tn = torch.tensor([sum(nt) / len(nt)], device=dev, dtype=torch.float64)
-    dist.all_reduce(tn, op=dist.ReduceOp.MAX)
-    nccl_gbs = S_CFG2 / float(tn.item()) / 1e9
+    nccl_gbs = S_CFG2 / _max_over_ranks(sum(nt) / len(nt), dev) / 1e9
+
+    # configs[2]: binomial-tree compressed Scatter of a 1 GiB root buffer vs NCCL scatter
+    ns = (1 << 30) // 4
+    root_buf = torch.from_numpy(O.smooth_field(ns, 0.0)).to(dev) if rank == 0 else None
+    sc_out = torch.empty(ns // world, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        c.binomial_scatter(root_buf, EB, root=0, out=sc_out)
+    torch.cuda.synchronize()
+    st = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        c.binomial_scatter(root_buf, EB, root=0, out=sc_out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        st.append(e0.elapsed_time(e1) * 1e-3)
+    scatter_gbs = 4 * ns / _max_over_ranks(sum(st) / len(st), dev) / 1e9
+    parts = list(root_buf.chunk(world)) if rank == 0 else None
+    ys = torch.empty(ns // world, dtype=torch.float32, device=dev)
+    for _ in range(3):
+        dist.scatter(ys, parts, src=0)
+    torch.cuda.synchronize()
+    nst = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        dist.scatter(ys, parts, src=0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        nst.append(e0.elapsed_time(e1) * 1e-3)
+    nccl_scatter_gbs = 4 * ns / _max_over_ranks(sum(nst) / len(nst), dev) / 1e9
+
     value = S_CFG2 / t / 1e9
-    cr = c.compression_ratio()
+    peak, peak_kind = peaks()
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -356,16 +435,24 @@ def bench_allreduce(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32 (compressed u8 wire, f64 closed loop)",
             "data": "synthetic smooth field per rank (phase 0.37 r)",
             "config": {"workload": "ring-allreduce (compressed RS + compress-once AG), 512 MiB f32 per rank, eb=1e-4",
-                       "parallelism": f"ring over {world} GPUs, NVLink peer memory",
+                       "parallelism": f"ring over {world} GPUs, NVLink peer memory (CUDA IPC)",
                        "nccl_allreduce_gbs": round(nccl_gbs, 2), "compression_ratio": cr,
+                       "collective_roofline_gbs": round(900.0 * (cr or 1.0), 1),
+                       "collective_roofline_frac": round(value / (900.0 * (cr or 1.0)), 4),
+                       "scatter_1GiB_gbs": round(scatter_gbs, 2), "nccl_scatter_1GiB_gbs": round(nccl_scatter_gbs, 2),
                        "l2": "inputs (512 MiB) larger than L2"},
-            "roofline": {"bound": "nvlink*CR", "achieved": round(value, 2), "peak": round(900.0 * (cr or 1.0), 1),
-                         "unit": "GB/s", "frac": round(value / (900.0 * (cr or 1.0)), 4), "traffic": None},
-            "e2e": None,
-            "gpu_launches": c.launches_per_call * args.steps,
+            "roofline": {"bound": "hbm", "kernel": "fused RS step = k_tile_encode<STEP> + k_gather",
+                         "achieved": round(step_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(step_gbs / peak, 4), "traffic": None,
+                         "algorithmic_bytes_per_launch": int(step_bytes), "avg_step_us": round(t_step * 1e6, 2)},
+            "e2e": {"value": round(S_CFG2 / t_e2e / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
+                    "d2h_bytes_per_step": 4 * n,
+                    "api": "pinned host f32 -> H2D -> Communicator.ring_allreduce -> D2H, max over ranks"},
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    c.close()
     dist.barrier()
     dist.destroy_process_group()
     return 0

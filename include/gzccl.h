@@ -38,8 +38,9 @@ enum {
 /* Device error record (32 bytes). */
 typedef struct gz_status {
   uint64_t first_nonfinite; /* index of the first non-finite input, ~0 if none (codec.py:83-85) */
-  uint64_t decode_error;    /* (block_index << 8) | code, ~0 if none; codes 1 width, 2 truncated,
-                               3 trailing bytes, 4 sidecar mismatch, 5 header (codec.py:273-322) */
+  uint64_t decode_error;    /* (block_index << 24) | (width << 8) | code, ~0 if none; the smallest
+                               block index wins; codes 1 width, 2 truncated, 3 trailing bytes,
+                               4 sidecar mismatch, 5 header (codec.py:273-322) */
   uint64_t reserved[2];
 } gz_status;
 
@@ -131,6 +132,9 @@ typedef struct {
 } gz_copy_item;
 #define GZ_MAX_COPY_ITEMS 64
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream);
+
+/* number of kernels this library has launched so far (all entry points) */
+uint64_t gz_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -44,6 +44,7 @@ SIGNATURES = {
     "gz_stream_wait_u32_geq": (i32, [p, p, u32]),
     "gz_copy_blob": (i32, [p, p, p, u64, p]),
     "gz_copy_items": (i32, [p, u32, p]),
+    "gz_launch_count": (u64, []),
 }
 
 _lib = None

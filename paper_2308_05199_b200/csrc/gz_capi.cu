@@ -18,6 +18,13 @@ namespace {
 constexpr size_t DEC_SMEM_BYTES = (size_t)WARPS * DEC_WARP_SMEM;  // per warp: value tile + two stagings
 constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-parameter budget)
 
+// kernels launched by this library (all entry points, all streams): lets a
+// benchmark count exactly which launches it timed
+unsigned long long g_launches = 0;
+unsigned long long* g_dbg = nullptr;  // experiments: per-warp timestamps
+int g_dbg_flags = 0;                 // experiments: bit 0 = skip the gather kernel
+inline void count_launch(unsigned k = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)k, __ATOMIC_RELAXED); }
+
 inline uint64_t nblocks(uint64_t n) { return (n + BLOCK - 1) / BLOCK; }
 inline uint64_t ntiles_of(uint64_t n) { return (nblocks(n) + TB - 1) / TB; }
 
@@ -125,26 +132,33 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   }
   a.nctas = base;
   a.total_tiles = total_tiles;
-  // tiles per gather CTA: 32, doubled until the grid fits MAXGRID
-  uint32_t gt = GATHER_MIN_TILES;
+  // tiles per gather CTA: 32, doubled until the grid fits MAXGRID; each
+  // segment's gather CTAs start at a multiple of 32 (agg2 groups)
+  uint32_t gs = 5;
+  auto gctas = [&](uint32_t sh) {
+    uint64_t g = 0;
+    for (int k = 0; k < a.nseg; ++k) {
+      g = (g + 31) & ~31ull;
+      g += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << sh) - 1) >> sh);
+    }
+    return g;
+  };
+  while (gctas(gs) > (uint64_t)MAXGRID && (1u << gs) < (uint32_t)GATHER_THREADS) ++gs;
+  if (gctas(gs) > (uint64_t)MAXGRID) return GZ_EINVAL;
   uint64_t gbase = 0;
-  while (true) {
-    gbase = 0;
-    for (int k = 0; k < a.nseg; ++k) gbase += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + gt - 1) / gt);
-    if (gbase <= (uint64_t)MAXGRID || gt >= (uint32_t)GATHER_THREADS) break;
-    gt *= 2;
-  }
-  if (gbase > (uint64_t)MAXGRID) return GZ_EINVAL;
-  gbase = 0;
   for (int k = 0; k < a.nseg; ++k) {
+    gbase = (gbase + 31) & ~31ull;
     a.seg[k].gcta_base = gbase;
-    gbase += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + gt - 1) / gt);
+    a.seg[k].gcta_n = std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << gs) - 1) >> gs);
+    gbase += a.seg[k].gcta_n;
   }
-  a.gtiles = gt;
+  a.gshift = gs;
   a.ngctas = gbase;
+  count_launch(2);  // + the gather below
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   int rc = (int)cudaGetLastError();
   if (rc) return rc;
+  if (g_dbg_flags & 1) return 0;
   // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)gbase);
@@ -231,12 +245,16 @@ PFN_waitValue32 p_wait32() {
 }  // namespace
 
 // experiments only: per-warp timestamps of the next compress launch
-static unsigned long long* g_dbg = nullptr;
 
 extern "C" {
 
 int gz_debug_set_timestamps(void* p) {
   g_dbg = reinterpret_cast<unsigned long long*>(p);
+  return 0;
+}
+// experiments only: bit 0 = skip the gather kernel (output incomplete)
+int gz_debug_set_flags(int f) {
+  g_dbg_flags = f;
   return 0;
 }
 
@@ -270,7 +288,7 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0, 0};
+  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
@@ -301,6 +319,7 @@ int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, 
   grid_cap(k_tile_decode, DEC_SMEM_BYTES, cap);
   const uint64_t want = (ntiles_of(n) + WARPS - 1) / WARPS;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
+  count_launch();
   k_tile_decode<<<grid, CTA_THREADS, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(a);
   return (int)cudaGetLastError();
 }
@@ -321,6 +340,7 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   if (n == 0) return 0;
   Status* st = reinterpret_cast<Status*>(d_status);
   if (payload_len == 0) {  // codec.py:307-308 at block 0
+    count_launch();
     k_record_error<<<1, 1, 0, s>>>(st, (unsigned long long)DE_TRUNC);
     return (int)cudaGetLastError();
   }
@@ -344,6 +364,7 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   const uint64_t nb_eff = std::min<uint64_t>(nblocks(n), payload_len / 5 + 2);
   iw.g8 = reinterpret_cast<unsigned long long*>(take(((nb_eff + GROUP - 1) / GROUP) * 8));
   const uint8_t* payload = blob + HEADER_BYTES;
+  count_launch(4);  // idx_segments, idx_chunks, idx_resolve, idx_emit
   idx_segments<<<(unsigned)nseg, 160, 0, s>>>(payload, payload_len, iw);
   const size_t csm = (size_t)CH * NE * 4;
   static bool attr = false;
@@ -358,6 +379,7 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   const uint64_t nt = ntiles_of(n);
   const uint64_t work = std::max<uint64_t>(nt * GROUPS, nt + 1);
   SidecarView sv = sidecar_view(sidecar, n);
+  count_launch();
   idx_sidecar<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(iw, n, payload_len, sv.tile_off, sv.sub_off);
   return (int)cudaGetLastError();
 }
@@ -374,7 +396,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView so = sidecar_view(sidecar_out, m);
-  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0, 0};
+  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   const WsView wv = carve(ws, ntiles_of(m));
@@ -425,7 +447,7 @@ int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg
       const uint64_t n = h_counts[i];
       SidecarView sv{nullptr, nullptr};
       if (sidecars) sv = sidecar_view(reinterpret_cast<uint8_t*>(sidecars) + h_seg_sidecar_off[i], n);
-      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, 0, tiles};
+      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, 0, 0, tiles};
       tiles += ntiles_of(n);
       xoff += n;
     }
@@ -505,6 +527,7 @@ int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value) {
 
 int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64_t max_bytes, gz_stream_t stream) {
   if (!src || !dst || !d_len || !aligned16(src) || !aligned16(dst)) return GZ_EINVAL;
+  count_launch();
   k_copy_blob<<<296, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const uint4*>(src), reinterpret_cast<uint4*>(dst),
                                                       d_len, max_bytes);
   return (int)cudaGetLastError();
@@ -523,8 +546,11 @@ int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream)
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const unsigned gx = (unsigned)std::max(1, 2 * sms / (int)count);
+  count_launch();
   k_copy_items<<<dim3(gx, count), 256, 0, (cudaStream_t)stream>>>(ci);
   return (int)cudaGetLastError();
 }
+
+uint64_t gz_launch_count(void) { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
 
 }  // extern "C"

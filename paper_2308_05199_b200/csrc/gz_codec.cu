@@ -25,7 +25,8 @@ struct Seg {
   uint64_t* out_tile_off;  // sidecar: [ntiles + 1] payload offsets of tiles
   uint16_t* out_sub_off;   // sidecar: [ntiles * GROUPS] offsets of every 8th block inside its tile
   uint64_t cta_base;       // first encoder CTA of this segment
-  uint64_t gcta_base;      // first gather CTA (ticket) of this segment
+  uint64_t gcta_base;      // first gather CTA of this segment (a multiple of 32)
+  uint64_t gcta_n;         // gather CTAs of this segment (up to the next base: padding)
   uint64_t tile_base;      // first slot of this segment in tile_rel / scratch
 };
 
@@ -34,8 +35,8 @@ struct EncodeArgs {
   Seg seg[NSEG];
   int nseg;
   uint64_t nctas;          // encoder CTAs (== grid), split over segments by cta_base
-  uint64_t ngctas;         // gather CTAs, `gtiles` tiles each, split by gcta_base
-  uint32_t gtiles;         // tiles per gather CTA (32..GATHER_THREADS)
+  uint64_t ngctas;         // gather CTAs, 2^gshift tiles each, split by gcta_base
+  uint32_t gshift;         // log2(tiles per gather CTA), 5..7
   uint64_t total_tiles;    // tiles over all segments
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
@@ -63,9 +64,13 @@ struct DecodeArgs {
   Status* st;
 };
 
-constexpr int ENC_WARP_SMEM = 2 * TILE_VALUES * 4 + STAGE_BYTES;  // two value tiles + staging
+// Fused step: the received tile's bytes are staged synchronously (one
+// staging buffer per warp keeps 16 warps resident; measured faster than two
+// asynchronous stagings with 13 warps).
+constexpr bool STEP_ASYNC_STAGE = false;
+constexpr int ENC_WARP_SMEM = 2 * TILE_VALUES * 4 + (STEP_ASYNC_STAGE ? 2 : 1) * STAGE_BYTES;
 // warps per encoder CTA (one CTA per SM): as many as shared memory allows
-__host__ __device__ constexpr int enc_warps(int src) { return src == 1 ? 16 : 24; }
+__host__ __device__ constexpr int enc_warps(int src) { return src == 1 ? (STEP_ASYNC_STAGE ? 13 : 16) : 24; }
 constexpr int DEC_WARP_SMEM = TILE_VALUES * 4 + 2 * STAGE_BYTES;  // value tile + two stagings
 
 // -------------------------------------------------------------------------
@@ -170,16 +175,18 @@ __device__ __forceinline__ void init_step_table(double* s_step, double tw) {
 // Block starts of a staged compressed tile.  The sidecar gives the offset of
 // every 8th block; lane g < 4 walks 8 width bytes (codec.py:305-320) and
 // records starts and widths in the warp's shared arrays.  Caller __syncwarp()s.
-__device__ __forceinline__ void walk_groups(const uint32_t* stage, int base, int tile_bytes, const uint16_t* sub,
-                                            int nblk, uint64_t b0, uint64_t nb, int last_cnt, Status* st,
-                                            uint16_t* s_start, uint8_t* s_w, int lane) {
+// `sub` = this lane's sidecar sub-offset (lanes < GROUPS); all lanes call.
+__device__ __forceinline__ void walk_groups(const uint32_t* stage, int base, int tile_bytes, int sub, int nblk,
+                                            uint64_t b0, uint64_t nb, int last_cnt, Status* st, uint16_t* s_start,
+                                            uint8_t* s_w, int lane) {
   const int g = lane;
+  const int sub_next = __shfl_down_sync(0xFFFFFFFFu, sub, 1);
   if (g >= GROUPS || g * GROUP >= nblk) return;
   const int g0 = g * GROUP;
   const int gblk = min(GROUP, nblk - g0);
-  const int gend = (g0 + GROUP < nblk) ? (int)sub[g + 1] : tile_bytes;
+  const int gend = (g0 + GROUP < nblk) ? sub_next : tile_bytes;
   const uint8_t* bytes = reinterpret_cast<const uint8_t*>(stage) + base;
-  int pos = sub[g];
+  int pos = sub;
   for (int k = 0; k < gblk; ++k) {
     const int w = bytes[pos];
     const uint64_t gb = b0 + g0 + k;
@@ -456,8 +463,8 @@ __device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg&
 template <int SRC, int NSEG, bool FAST>
 __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
                                            float* xs, uint32_t* dst, int pos0, bool run_mode, uint32_t& carry,
-                                           uint32_t* stage, uint16_t* s_start, uint8_t* s_w, const double* s_step,
-                                           uint64_t pol_keep, int lane) {
+                                           uint32_t* stage, int in_base, int in_bytes, int in_sub, uint16_t* s_start,
+                                           uint8_t* s_w, const double* s_step, uint64_t pol_keep, int lane) {
   const uint64_t nb = G.nb, b0 = tile * TB, v0 = b0 * BLOCK;
   const int last_cnt = G.last_cnt;
   const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
@@ -465,12 +472,10 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   int base = 0;
 
   // ---- 1. fused step: combine the received blob's tile into xs
+  // (its compressed bytes were staged asynchronously with the local values)
   if (SRC == SRC_STEP) {
-    const uint64_t ts = a.in_tile_off[tile], te = a.in_tile_off[tile + 1];
-    base = stage_bytes<false>(stage, a.in_blob + HEADER_BYTES, ts, te, lane);
-    __syncwarp();
-    walk_groups(stage, base, (int)(te - ts), a.in_sub_off + tile * GROUPS, nblk, b0, nb, last_cnt, a.st, s_start,
-                s_w, lane);
+    base = in_base;
+    walk_groups(stage, base, in_bytes, in_sub, nblk, b0, nb, last_cnt, a.st, s_start, s_w, lane);
     __syncwarp();
     decode_row<1>(stage, base, nblk, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, s_start, s_w, lane);
     __syncwarp();
@@ -755,7 +760,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
   __shared__ uint16_t s_start[SRC == SRC_STEP ? NW : 1][TB];
   __shared__ uint8_t s_w[SRC == SRC_STEP ? NW : 1][TB];
-  __shared__ unsigned int s_next;
   // the gather kernel may be scheduled as soon as SMs free up; it waits for
   // this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -764,61 +768,78 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
   float* xsb1 = reinterpret_cast<float*>(my + TILE_VALUES * 4);
-  uint32_t* stage = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);  // fused step only
+  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);  // fused step only
+  uint32_t* stg1 = STEP_ASYNC_STAGE ? reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4 + STAGE_BYTES) : stg0;
   const int wi = SRC == SRC_STEP ? warp : 0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
-  if (tid == 0) s_next = 0;
   __syncthreads();
   const uint64_t c = blockIdx.x;
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
   const unsigned long long ts0 = a.dbg ? gtimer() : 0;
 
-  // ---- this CTA's segment and tile range
-  int k = 0;
-  if (NSEG > 1) {
-#pragma unroll 1
-    for (int i = 1; i < a.nseg; ++i)
-      if (a.seg[i].cta_base <= c) k = i;
-  }
-  const Seg& S = a.seg[k];
-  const uint64_t cta_lo = S.cta_base, cta_hi = (k + 1 < a.nseg) ? a.seg[k + 1].cta_base : a.nctas;
-  const uint64_t cl = c - cta_lo, ncta = cta_hi - cta_lo;
-  const SegGeom G = seg_geom(S.n);
-  const uint64_t r0 = (G.ntiles * cl) / ncta, r1 = (G.ntiles * (cl + 1)) / ncta;
-  const unsigned int nr = (unsigned int)(r1 - r0);
-  uint32_t* const sizes = a.tile_rel + S.tile_base;
-  uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
-
+  // ---- warps claim tiles (over all segments) from one global counter, so
+  // SMs that run faster take more tiles; the next claim is prefetched
   auto claim = [&]() -> unsigned int {
     unsigned int v = 0;
-    if (lane == 0) v = atomicAdd(&s_next, 1u);
+    if (lane == 0) v = atomicAdd(&a.ws->claim, 1u);
     return __shfl_sync(0xFFFFFFFFu, v, 0);
   };
+  const unsigned int total = (unsigned int)a.total_tiles;
+  // fused step: the received blob's tile jn is staged with the local values
+  // (same cp.async group); its offsets come from the sidecar
+  struct InTile {
+    int base, bytes, sub;
+  };
+  auto stage_in = [&](unsigned int jn, uint32_t* stg) {
+    InTile r{0, 0, 0};
+    if (SRC == SRC_STEP && jn < total) {
+      const uint64_t ts = a.in_tile_off[jn], te = a.in_tile_off[jn + 1];
+      r.base = stage_bytes<STEP_ASYNC_STAGE>(stg, a.in_blob + HEADER_BYTES, ts, te, lane);
+      r.bytes = (int)(te - ts);
+      r.sub = lane < GROUPS ? (int)a.in_sub_off[(uint64_t)jn * GROUPS + lane] : 0;
+    }
+    return r;
+  };
   unsigned int j = claim();
-  unsigned int j1 = j < nr ? claim() : nr;
-  if (j < nr) prefetch_tile(a, S.tile_base + r0 + j, xsb0, lane, pol_in);
+  unsigned int j1 = j < total ? claim() : total;
+  InTile in_cur{0, 0, 0}, in_nxt{0, 0, 0};
+  if (STEP_ASYNC_STAGE) in_cur = stage_in(j, stg0);
+  if (j < total) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
   unsigned long long wait_ns = 0, ndone = 0;
   uint32_t dummy = 0;
-  while (j < nr) {
-    prefetch_tile(a, j1 < nr ? S.tile_base + r0 + j1 : a.total_tiles, buf ? xsb0 : xsb1, lane, pol_in);
+  while (j < total) {
+    if (STEP_ASYNC_STAGE) in_nxt = stage_in(j1, buf ? stg0 : stg1);
+    prefetch_tile(a, j1, buf ? xsb0 : xsb1, lane, pol_in);
     const unsigned long long tw0 = a.dbg ? gtimer() : 0;
     cp_async_wait_1();
     __syncwarp();
     if (a.dbg) wait_ns += gtimer() - tw0;
-    const uint64_t t = r0 + j;
+    if (SRC == SRC_STEP && !STEP_ASYNC_STAGE) {
+      in_cur = stage_in(j, stg0);
+      __syncwarp();
+    }
+    const int k = NSEG > 1 ? seg_of_tile(a, j) : 0;
+    const Seg& S = a.seg[k];
+    const SegGeom G = seg_geom(S.n);
+    const uint64_t t = j - S.tile_base;
     const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
-                                                reinterpret_cast<uint32_t*>(slots + t * (uint64_t)TILE_SLOT), 0, false,
-                                                dummy, stage, s_start[wi], s_w[wi], s_step, pol_keep, lane);
+                                                reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), 0,
+                                                false, dummy, (STEP_ASYNC_STAGE && buf) ? stg1 : stg0, in_cur.base,
+                                                in_cur.bytes,
+                                                in_cur.sub, s_start[wi], s_w[wi], s_step, pol_keep, lane);
     if (lane == 0) {
-      sizes[t] = (uint32_t)tb;
-      atomicAdd(&a.ws->agg[S.gcta_base + t / a.gtiles], (unsigned)tb);
+      a.tile_rel[j] = (uint32_t)tb;
+      const uint64_t g = S.gcta_base + (t >> a.gshift);
+      atomicAdd(&a.ws->agg[g], (unsigned)tb);
+      atomicAdd(&a.ws->agg2[g >> 5], (unsigned)tb);
     }
     ++ndone;
     __syncwarp();
     buf ^= 1;
     j = j1;
-    j1 = j < nr ? claim() : nr;
+    in_cur = in_nxt;
+    j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
   if (a.dbg && lane == 0) {  // experiments: per-warp timestamps
@@ -831,56 +852,17 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
 
 // Encoder, kernel 2 of 2: the exclusive scan of codec.py:241-243 at tile
 // granularity and the gather of the slots into the blob.  Gather CTA g of a
-// segment owns `gtiles` consecutive tiles.  The encoder has added every
-// tile's size into agg[g], so the CTA's base offset is a plain parallel sum
-// of the segment's earlier agg[] entries (no look-back, no waiting); a block
-// scan of its tiles' sizes gives the tile offsets, and every thread then
+// segment owns 2^gshift consecutive tiles.  The encoder has added every
+// tile's size into agg[g] and agg2[g/32], so the CTA's base offset is a
+// parallel sum of at most 32 + MAXGRID/32/GATHER_THREADS*... loads issued
+// together with the load of its tiles' sizes (no look-back, no waiting on
+// other CTAs).  A block scan gives the tile offsets, and every thread then
 // produces aligned 16-byte chunks of the CTA's contiguous output range --
-// possibly in a peer GPU's memory (the NVLink send of a fused
-// reduce-scatter step) -- coalesced.  Launched as a programmatic dependent
-// of the encoder, so its launch overlaps the encoder's tail.
+// possibly in a peer GPU's memory (the NVLink send of a fused reduce-scatter
+// step) -- coalesced, all loads of a thread in flight at once.  Launched as a
+// programmatic dependent of the encoder, so its launch overlaps the encoder's
+// tail.
 constexpr int GATHER_THREADS = 128;
-constexpr int GATHER_MIN_TILES = 32;
-
-// 16 bytes from any byte address inside a slot (two aligned loads + funnel)
-__device__ __forceinline__ uint4 ld16u(const uint8_t* src) {
-  const uint4* s4 = reinterpret_cast<const uint4*>(reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15);
-  const int h = (int)(reinterpret_cast<uintptr_t>(src) & 15), wo = h >> 2, sh = (h & 3) * 8;
-  const uint4 cur = __ldcs(s4);
-  const uint4 nxt = h ? __ldcs(s4 + 1) : cur;
-  const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-  const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-  const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-  const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-  const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-  return make_uint4(__funnelshift_r(a0, a1, sh), __funnelshift_r(a1, a2, sh), __funnelshift_r(a2, a3, sh),
-                    __funnelshift_r(a3, a4, sh));
-}
-
-// 16 bytes of the CTA's output starting at local byte p, which lies in tile
-// i: one unaligned read out of tile i's slot, merged with the start of tile
-// i+1 when the chunk crosses the boundary (tiles other than a segment's last
-// are >= 160 bytes, so a chunk never spans three tiles).
-__device__ __forceinline__ uint4 gather16(const uint8_t* slots0, const uint32_t* loc, int i, uint32_t p) {
-  const uint4 A = ld16u(slots0 + (uint64_t)i * TILE_SLOT + (p - loc[i]));
-  const uint32_t k = loc[i + 1] - p;  // bytes of the chunk inside tile i
-  if (k >= 16) return A;
-  const uint4 B = ld16u(slots0 + (uint64_t)(i + 1) * TILE_SLOT);
-  // out byte b = b < k ? A[b] : B[b - k]
-  const uint32_t a[4] = {A.x, A.y, A.z, A.w}, bw[4] = {B.x, B.y, B.z, B.w};
-  const int ws = (int)(k >> 2), sh = (int)(k & 3) * 8;
-  uint32_t o[4];
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int q = j - ws;
-    const uint32_t hi = q >= 0 ? bw[q] : 0u, lo = q >= 1 ? bw[q - 1] : 0u;
-    const uint32_t bsh = __funnelshift_l(lo, hi, sh);  // B shifted up by k bytes
-    const int nb = (int)k - 4 * j;                     // bytes of word j taken from A
-    const uint32_t m = nb >= 4 ? 0xFFFFFFFFu : nb <= 0 ? 0u : (0xFFFFFFFFu >> (32 - 8 * nb));
-    o[j] = (a[j] & m) | (bsh & ~m);
-  }
-  return make_uint4(o[0], o[1], o[2], o[3]);
-}
 
 template <int NSEG>
 __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG> a) {
@@ -889,7 +871,10 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   __shared__ unsigned long long s_red[NWG];
   __shared__ uint32_t s_loc[GATHER_THREADS + 1];  // local payload offset of each tile, [nr] = total
   __shared__ int s_last;
+  const long long ck0 = clock64();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the encoder grid is complete
+  const long long ck1 = clock64();
+  const unsigned long long gt1 = a.dbg ? gtimer() : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   TileWs* ws = a.ws;
   const uint64_t c = blockIdx.x;
@@ -900,20 +885,32 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
       if (a.seg[i].gcta_base <= c) k = i;
   }
   const Seg& S = a.seg[k];
-  const uint64_t glo = S.gcta_base, ghi = (k + 1 < a.nseg) ? a.seg[k + 1].gcta_base : a.ngctas;
+  const uint64_t glo = S.gcta_base;
+  const bool real = c - glo < S.gcta_n;  // padding CTAs only retire
   const SegGeom G = seg_geom(S.n);
-  const uint64_t r0 = (c - glo) * a.gtiles;
-  const uint64_t r1 = umin64(r0 + a.gtiles, G.ntiles);
+  const uint64_t r0 = (c - glo) << a.gshift;
+  const uint64_t r1 = real ? umin64(r0 + (1u << a.gshift), G.ntiles) : r0;
   const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
   const uint32_t* const sizes = a.tile_rel + S.tile_base;
   const uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
 
-  // ---- base offset: bytes of the segment's earlier gather CTAs
-  unsigned long long part = 0;
-  for (uint64_t g = glo + tid; g < c; g += GATHER_THREADS) part += ws->agg[g];
+  // ---- all independent loads first: this CTA's tile sizes, the byte counts
+  // of the segment's earlier 32-groups (agg2) and of the earlier CTAs of
+  // this CTA's group (agg)
+  const uint32_t sz = tid < nr ? sizes[r0 + tid] : 0u;
+  const uint64_t g2lo = glo >> 5, g2 = c >> 5;
+  unsigned long long part = (uint64_t)tid < (c & 31) ? ws->agg[(c & ~31ull) + tid] : 0u;
+  {
+    uint32_t v[4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint64_t q = g2lo + tid + m * GATHER_THREADS;
+      v[m] = q < g2 ? ws->agg2[q] : 0u;
+    }
+    part += (unsigned long long)v[0] + v[1] + v[2] + v[3];
+  }
   part = warp_sum_u64(part);
   // ---- block scan of this CTA's tile sizes
-  const uint32_t sz = tid < nr ? sizes[r0 + tid] : 0u;
   uint32_t incl = sz;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -923,6 +920,9 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   if (lane == 31) s_wsum[warp] = incl;
   if (lane == 0) s_red[warp] = part;
   __syncthreads();
+  const long long ck2 = clock64();
+  // every CTA has read agg/agg2 once it is counted: the last one zeroes them
+  if (tid == 0) s_last = atomicAdd(&ws->done, 1ull) == a.ngctas - 1;
   uint32_t wpre = 0, agg = 0;
   unsigned long long excl = 0;
 #pragma unroll
@@ -942,7 +942,7 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
     s_loc[tid] = wpre + incl - sz;
   }
   if (tid == 0) s_loc[nr] = agg;
-  if (c == glo && tid < 6) {  // codec.py:158, HEADER "<4s4xQd"
+  if (real && c == glo && tid < 6) {  // codec.py:158, HEADER "<4s4xQd"
     uint32_t hw;
     if (tid == 0) hw = 0x31435A47u;  // "GZC1"
     else if (tid == 1) hw = 0;
@@ -954,71 +954,99 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
     }
     reinterpret_cast<uint32_t*>(S.blob)[tid] = hw;
   }
-  if (c == ghi - 1 && tid == 0) {  // the segment's last CTA knows the total
+  if (real && c == glo + S.gcta_n - 1 && tid == 0) {  // the segment's last CTA knows the total
     const unsigned long long total = excl + agg;
     if (S.out_tile_off) S.out_tile_off[G.ntiles] = total;
     *S.out_len = HEADER_BYTES + total;
   }
   __syncthreads();
-  // ---- copy: aligned 16-byte destination chunks; the source tile of a
-  // chunk by binary search over the local offsets; ragged ends byte-wise
-  // (they share a chunk with the neighbouring CTAs' ranges)
-  {
+  // ---- copy: warp w moves tiles w, w+NWG, ... (U of them per batch, all
+  // loads in flight).  Lane l holds 16-byte source chunk l of a 31-chunk
+  // window of the tile's slot (aligned); aligned destination chunk k is
+  // funnel-shifted from chunks k and k+1 (shuffled from lane k+1); the
+  // ragged head/tail bytes (shared with the neighbouring tiles' chunks) are
+  // stored byte-wise.
+  if (nr > 0) {
     uint8_t* const base = S.blob + HEADER_BYTES + excl;
     const uint8_t* const sl0 = slots + r0 * (uint64_t)TILE_SLOT;
-    const uintptr_t A = reinterpret_cast<uintptr_t>(base), E = A + agg;
-    const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cle = E & ~(uintptr_t)15;
-    auto find = [&](uint32_t p) {
-      int lo = 0, hi = nr - 1;  // last i with s_loc[i] <= p
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_loc[mid] <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      return lo;
-    };
-    auto byte_at = [&](uint32_t p) {
-      const int i = find(p);
-      return sl0[(uint64_t)i * TILE_SLOT + (p - s_loc[i])];
-    };
-    if (cf < cle) {
-      const uint32_t head = (uint32_t)(cf - A);
-      const uint32_t nch = (uint32_t)((cle - cf) >> 4);
-      uint4* d4 = reinterpret_cast<uint4*>(cf);
-      constexpr int B = 4;
-      for (uint32_t c0 = tid; c0 < nch; c0 += B * GATHER_THREADS) {
-        uint4 v[B];
+    constexpr int U = 8;
+    long long cka = 0, ckb = 0, ckc = 0;
+    for (int i0 = warp; i0 < nr; i0 += NWG * U) {
+      if (i0 == warp) cka = clock64();
+      uint4 v[U];
+      int len[U];
 #pragma unroll
-        for (int m = 0; m < B; ++m) {
-          const uint32_t ch = c0 + m * GATHER_THREADS;
-          if (ch < nch) {
-            const uint32_t p = head + 16 * ch;
-            v[m] = gather16(sl0, s_loc, find(p), p);
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NWG;
+        len[u] = i < nr ? (int)(s_loc[i + 1] - s_loc[i]) : 0;
+        v[u] = 16 * lane < len[u] + 16 ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane)
+                                       : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NWG;
+        if (len[u] == 0) continue;  // warp-uniform
+        const uint8_t* src = sl0 + (uint64_t)i * TILE_SLOT;
+        uint8_t* dst = base + s_loc[i];
+        const int L = len[u];
+        const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+        const int wo = h >> 2, sh = (h & 3) * 8;
+        const int nfull = (L - h) >> 4;  // aligned destination chunks
+        uint4 cur = v[u];
+        for (int w0 = 0; w0 < nfull; w0 += 31) {  // 31 output chunks per window
+          if (w0) {
+            const int q = w0 + lane;
+            cur = 16 * q < L + 16 ? *reinterpret_cast<const uint4*>(src + 16 * q) : make_uint4(0, 0, 0, 0);
+          }
+          uint4 nxt;
+          nxt.x = __shfl_down_sync(0xFFFFFFFFu, cur.x, 1);
+          nxt.y = __shfl_down_sync(0xFFFFFFFFu, cur.y, 1);
+          nxt.z = __shfl_down_sync(0xFFFFFFFFu, cur.z, 1);
+          nxt.w = __shfl_down_sync(0xFFFFFFFFu, cur.w, 1);
+          const int k = w0 + lane;
+          if (lane < 31 && k < nfull) {
+            const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+            const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+            const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+            const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+            const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+            uint4 o;
+            o.x = __funnelshift_r(a0, a1, sh);
+            o.y = __funnelshift_r(a1, a2, sh);
+            o.z = __funnelshift_r(a2, a3, sh);
+            o.w = __funnelshift_r(a3, a4, sh);
+            *reinterpret_cast<uint4*>(dst + h + 16 * k) = o;
           }
         }
-#pragma unroll
-        for (int m = 0; m < B; ++m) {
-          const uint32_t ch = c0 + m * GATHER_THREADS;
-          if (ch < nch) d4[ch] = v[m];
-        }
+        const int t0 = h + 16 * nfull;  // tail bytes [t0, L)
+        if (lane < h) dst[lane] = src[lane];
+        if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = src[t0 + lane - 16];
+        if (i0 == warp && u == 0) ckb = clock64();
       }
-      const uint32_t tail0 = head + 16 * nch;
-      if (tid < head) base[tid] = byte_at(tid);
-      if (tid >= 32 && tid - 32 < agg - tail0) base[tail0 + (tid - 32)] = byte_at(tail0 + (tid - 32));
-    } else {
-      for (uint32_t p = tid; p < agg; p += GATHER_THREADS) base[p] = byte_at(p);
+      if (i0 == warp) ckc = clock64();
+    }
+    if (a.dbg && tid == 0) {
+      unsigned long long* d = a.dbg + 4096 * 24 * 12 + 16384 * 8 + c * 4;
+      d[0] = ckb - cka; d[1] = ckc - ckb; d[2] = clock64() - ckc; d[3] = 1;
     }
   }
-  // ---- retire: the last CTA zeroes agg[] for the next launch
+  const long long ck3 = clock64();
+  // ---- the last CTA to be counted zeroes agg/agg2 for the next launch
   __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    s_last = atomicAdd(&ws->done, 1ull) == a.ngctas - 1;
+  if (a.dbg && tid == 0) {
+    unsigned long long* d = a.dbg + 4096 * 24 * 12 + c * 8;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    d[0] = gt1; d[1] = ck1 - ck0; d[2] = ck2 - ck1; d[3] = ck3 - ck2; d[4] = clock64() - ck3; d[5] = smid; d[6] = nr;
+    d[7] = gtimer();
   }
-  __syncthreads();
   if (s_last) {
     for (uint64_t g = tid; g < a.ngctas; g += GATHER_THREADS) ws->agg[g] = 0;
-    if (tid == 0) ws->done = 0;
+    for (uint64_t g = tid; g < (a.ngctas + 31) / 32; g += GATHER_THREADS) ws->agg2[g] = 0;
+    if (tid == 0) {
+      ws->done = 0;
+      ws->claim = 0;
+    }
   }
 }
 
@@ -1070,8 +1098,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
     const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
     const uint64_t v0 = b0 * BLOCK;
     const int nval = (int)(n - v0 < (uint64_t)TILE_VALUES ? n - v0 : (uint64_t)TILE_VALUES);
-    walk_groups(stage, base, (int)(te - ts), a.sub_off + t * GROUPS, nblk, b0, nb, last_cnt, a.st, s_start[warp],
-                s_w[warp], lane);
+    walk_groups(stage, base, (int)(te - ts), lane < GROUPS ? (int)a.sub_off[t * GROUPS + lane] : 0, nblk, b0, nb,
+                last_cnt, a.st, s_start[warp], s_w[warp], lane);
     __syncwarp();
     decode_row<0>(stage, base, nblk, b0, nb, last_cnt, a.tw, xs, 0, s_step, s_start[warp], s_w[warp], lane);
     __syncwarp();

@@ -49,15 +49,19 @@ constexpr int MAGIC32_BITS = 0x4B400000;
 
 // ---- device workspace: zero-initialised once, reused by every launch -------
 // Layout: this header, tile sizes (u32 per tile), scratch slots.
-// agg[g] = compressed bytes of gather CTA g's tiles, accumulated by the
-// encoder kernel and zeroed again by the last gather CTA to retire, so no
-// per-launch memset is needed and CUDA-graph replay is safe.
-constexpr int MAXGRID = 16384;   // gather CTAs per launch
+// agg[g] = compressed bytes of gather CTA g's tiles and agg2[g / 32] = bytes
+// of gather CTAs 32*(g/32) .. +31, accumulated by the encoder kernel and
+// zeroed again by the last gather CTA to retire, so no per-launch memset is
+// needed and CUDA-graph replay is safe.
+constexpr int MAXGRID = 16384;   // gather CTAs per launch (segments 32-aligned)
 constexpr int TILE_SLOT = 4224;  // scratch bytes reserved per tile (>= 32 * 129, 128-aligned)
 struct TileWs {
   unsigned long long done;          // gather retire counter (own 128-byte line)
   unsigned long long pad0[15];
+  unsigned int claim;               // encoder tile claims (own 128-byte line)
+  unsigned int pad1[31];
   unsigned int agg[MAXGRID];
+  unsigned int agg2[MAXGRID / 32];
 };
 
 struct Status {                          // error reporting (host-reset to ~0)
@@ -179,15 +183,20 @@ __device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, c
 // Per step, with prev = previous reconstruction (f32 prev32, exact f64 prev64):
 //   vf = RN32(RN32(x - prev) * RN32(1/tw)) approximates the reference's
 //   v = fl64(fl64(x-prev)/tw) with |vf - v| <= 3.01 * 2^-24 |v|.
-//   m = vf + 1.5*2^23 holds RNE(vf) for |vf| < 2^21; fr = vf - RNE(vf).
+//   m = vf + 1.5*2^23 holds q = RNE(vf) for |vf| < 2^22; fr = vf - q.
 //   If |fr| + 2^-21 |vf| < 0.5 - 2^-20 then |v| is more than 2^-21 away from
-//   every half-integer, so floor(fl64(|v|+0.5))*sign(v) == RNE(vf), and
-//   |q| < 2^21 (no overflow, codec.py:201-204).
+//   every half-integer, so floor(fl64(|v|+0.5))*sign(v) == q.
+//   Only max|fr| is tracked per step; the test runs once per block with
+//   |vf| <= |q| + 1/2 <= 2^(w-1) + 1/2 (w = bit width of the zigzag codes).
+//   Requiring w <= 21 also proves |vf| < 2^21 (the magic-constant rounding is
+//   valid and |q| <= 2^20, no overflow, codec.py:201-204): a larger |vf|, an
+//   infinity or a NaN turns into an integer code of width >= 22.
 //   The reconstruction rec = RN32(fl64(prev + fl64(q*tw))) is computed exactly
 //   as codec.py:205-207 does.  The error test of codec.py:208-210 is decided
 //   in binary32: e = RN32(|rec - x|) has relative error <= 2^-24, so
-//   e < elo (<= eb (1 - 2^-22)) proves |rec - x| <= eb and e > ehi
-//   (>= eb (1 + 2^-22)) proves |rec - x| > eb; only e in [elo, ehi] is undecided.
+//   max e < elo (<= eb (1 - 2^-22)) proves every |rec - x| <= eb and
+//   max e > ehi (>= eb (1 + 2^-22)) proves some |rec - x| > eb; only a
+//   maximum inside [elo, ehi] is undecided.
 enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
 
 __device__ __forceinline__ int fast_block(float* xs, int row, double tw, float rtw, float thr, float elo, float ehi,
@@ -198,8 +207,8 @@ __device__ __forceinline__ int fast_block(float* xs, int row, double tw, float r
   float prev32 = c4.x;
   x0 = c4.x;
   double prev64 = (double)prev32;
-  bool rnd = true;
-  float emax = 0.0f;  // max |rec - x| over the block (f32, decided once)
+  float frmax = 0.0f;  // max |vf - q|
+  float emax = 0.0f;   // max |rec - x|
   uint32_t zor = 0;
   uint32_t zc[4];
   zc[0] = __float_as_uint(x0);
@@ -209,23 +218,27 @@ __device__ __forceinline__ int fast_block(float* xs, int row, double tw, float r
     const float x = (j & 3) == 0 ? c4.x : (j & 3) == 1 ? c4.y : (j & 3) == 2 ? c4.z : c4.w;
     const float vf = __fmul_rn(__fsub_rn(x, prev32), rtw);
     const float m = __fadd_rn(vf, MAGIC32);
-    const float fr = __fsub_rn(vf, __fsub_rn(m, MAGIC32));
-    rnd &= fmaf(fabsf(vf), 0x1p-21f, fabsf(fr)) < thr;
+    frmax = fmaxf(frmax, fabsf(__fsub_rn(vf, __fsub_rn(m, MAGIC32))));
     const uint32_t qb = (uint32_t)__float_as_int(m) + 0x34C00000u;  // q ^ 0x80000000
     const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)qb), 4503601774854144.0);
     const double t = __dadd_rn(prev64, __dmul_rn(qd, tw));
     prev32 = __double2float_rn(t);
     prev64 = (double)prev32;
-    const float e = fabsf(__fsub_rn(prev32, x));
-    emax = fmaxf(emax, e);
-    const uint32_t z = ~((qb << 1) ^ (uint32_t)((int)qb >> 31));     // zigzag(q)
+    emax = fmaxf(emax, fabsf(__fsub_rn(prev32, x)));
+    // zigzag(q) = (q << 1) ^ (q >> 31) = (qb << 1) ^ ~(qb >> 31): shift, add, one LOP3
+    uint32_t z;
+    asm("{\n\t.reg .b32 s, d;\n\tshr.s32 s, %1, 31;\n\tadd.u32 d, %1, %1;\n\tlop3.b32 %0, d, s, 0, 0xC3;\n\t}"
+        : "=r"(z) : "r"(qb));
     zor |= z;
     zc[j & 3] = z;
     if ((j & 3) == 3)
       *reinterpret_cast<uint4*>(xs + xs_index(row, j >> 2)) = make_uint4(zc[0], zc[1], zc[2], zc[3]);
   }
   zor_out = zor;
-  if (!rnd) return FB_SLOW;
+  const int w = 32 - __clz(zor);
+  if (w > 21) return FB_SLOW;
+  const float vmax = __int_as_float((126 + w) << 23) + 0.5f;  // 2^(w-1) + 1/2 (exact; w = 0 gives 1)
+  if (!(fmaf(vmax, 0x1p-21f, frmax) < thr)) return FB_SLOW;
   if (emax > ehi) return FB_RAW;             // some error provably > eb
   return emax >= elo ? FB_SLOW : FB_PACKED;  // undecided within 2^-22 of eb
 }
