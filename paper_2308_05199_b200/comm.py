@@ -101,6 +101,7 @@ class Communicator:
         self.last_compression_ratio = None
         self.launches_per_call = 0
         self.events = None  # list -> (label, cuda event) marks after every wait/launch (profiling)
+        self.copy_stream = torch.cuda.Stream(self.device)  # allgather pulls
 
     # ------------------------------------------------------------------ setup
     def _setup(self, n: int):
@@ -253,21 +254,56 @@ class Communicator:
                 if not p.last:
                     self._signal(p.dst, lay.rs_full(p.slot + 1), e, s)
                 else:
-                    # slots of this epoch fully consumed: tell the left neighbour;
                     # the owned blob is ready: tell every peer
-                    self._signal(left, lay.rs_consumed(), e, s)
                     for j in range(N):
                         if j != i:
                             self._signal(j, lay.ag_ready(i), e, s)
-            else:  # Gather: pull the owner's compress-once blob over NVLink
-                self._wait(lay.ag_ready(p.owner), e, s)
-                L.check(lib.gz_decompress_sidecar(self._addr(p.owner, lay.own_off[0]),
-                                                  self._addr(p.owner, lay.own_off[1]), msize(p.chunk), ebf,
-                                                  chunk_ptr(out, p.chunk), ws.status_ptr(), s),
-                        "gz_decompress_sidecar")
-                launches += 1
-                self._mark("decode")
-                self._signal(p.owner, lay.ag_consumed(i), e, s)
+        # compress-once allgather: a side stream pulls each owner's blob +
+        # sidecar over NVLink into our (now free) reduce-scatter slots with one
+        # bulk copy, and releases the owner; the main stream decodes it from
+        # local HBM as soon as it has landed, while the next copy is in flight
+        gathers = [p for p in ring_allreduce_plan(N, i) if not isinstance(p, (Compress, Reduce))]
+        if len(gathers) == 1:
+            # a single owner leaves nothing to overlap the copy with: decode
+            # straight out of its memory over NVLink
+            p = gathers[0]
+            self._wait(lay.ag_ready(p.owner), e, s)
+            L.check(lib.gz_decompress_sidecar(self._addr(p.owner, lay.own_off[0]), self._addr(p.owner, lay.own_off[1]),
+                                              msize(p.chunk), ebf, chunk_ptr(out, p.chunk), ws.status_ptr(), s),
+                    "gz_decompress_sidecar")
+            launches += 1
+            self._mark("decode")
+            self._signal(p.owner, lay.ag_consumed(i), e, s)
+            gathers = []
+        cs = self.copy_stream.cuda_stream
+        if gathers:
+            rs_done = torch.cuda.Event()
+            rs_done.record(self.stream)
+            self.copy_stream.wait_event(rs_done)
+        landed = []
+        for k, p in enumerate(gathers):
+            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(p.owner)), e), "gz_stream_wait_u32_geq")
+            b, sc = lay.slot_off[k]
+            items = (_CopyItem * 2)(
+                _CopyItem(self._addr(p.owner, lay.own_off[0]), self._addr(i, b),
+                          self._addr(p.owner, lay.len_off + 8 * N), lay.blob_cap),
+                _CopyItem(self._addr(p.owner, lay.own_off[1]), self._addr(i, sc), None,
+                          int(lib.gz_sidecar_bytes(msize(p.chunk)))))
+            L.check(lib.gz_copy_items(items, 2, cs), "gz_copy_items")
+            launches += 1
+            self._signal(p.owner, lay.ag_consumed(i), e, cs)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+            landed.append(ev)
+        for k, p in enumerate(gathers):
+            self.stream.wait_event(landed[k])
+            b, sc = lay.slot_off[k]
+            L.check(lib.gz_decompress_sidecar(self._addr(i, b), self._addr(i, sc), msize(p.chunk), ebf,
+                                              chunk_ptr(out, p.chunk), ws.status_ptr(), s), "gz_decompress_sidecar")
+            launches += 1
+            self._mark("decode")
+        # our slots are free again: the left neighbour may write the next call's steps
+        self._signal(left, lay.rs_consumed(), e, s)
         self.epoch = e
         self.launches_per_call = launches
         return out

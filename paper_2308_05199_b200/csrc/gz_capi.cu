@@ -192,21 +192,32 @@ struct CopyItems {
   gz_copy_item it[GZ_MAX_COPY_ITEMS];
 };
 
-// blockIdx.y = item; 16-byte body, byte tail.
+// blockIdx.y = item; 16-byte body (eight loads in flight per thread: the
+// source is usually a peer GPU, so the copy is latency-bound otherwise),
+// byte tail.
 __global__ void k_copy_items(const CopyItems ci) {
   const gz_copy_item& it = ci.it[blockIdx.y];
   const uint64_t len = it.d_len ? umin64(*it.d_len, it.max_bytes) : it.max_bytes;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   if (((reinterpret_cast<uintptr_t>(it.src) | reinterpret_cast<uintptr_t>(it.dst)) & 15) != 0) {
     // unaligned (small) item: byte copy
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < len; i += (uint64_t)gridDim.x * blockDim.x)
-      it.dst[i] = it.src[i];
+    for (uint64_t i = t0; i < len; i += stride) it.dst[i] = it.src[i];
     return;
   }
   const uint64_t nch = len >> 4;
   const uint4* s = reinterpret_cast<const uint4*>(it.src);
   uint4* d = reinterpret_cast<uint4*>(it.dst);
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nch; i += (uint64_t)gridDim.x * blockDim.x)
-    d[i] = __ldcs(s + i);
+  constexpr int B = 8;
+  for (uint64_t i0 = t0; i0 < nch; i0 += B * stride) {
+    uint4 v[B];
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (i0 + b * stride < nch) v[b] = __ldcs(s + i0 + b * stride);
+#pragma unroll
+    for (int b = 0; b < B; ++b)
+      if (i0 + b * stride < nch) d[i0 + b * stride] = v[b];
+  }
   if (blockIdx.x == 0 && threadIdx.x < (len & 15)) it.dst[(nch << 4) + threadIdx.x] = it.src[(nch << 4) + threadIdx.x];
 }
 
@@ -545,7 +556,7 @@ int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned gx = (unsigned)std::max(1, 2 * sms / (int)count);
+  const unsigned gx = (unsigned)std::max(1, 4 * sms / (int)count);
   count_launch();
   k_copy_items<<<dim3(gx, count), 256, 0, (cudaStream_t)stream>>>(ci);
   return (int)cudaGetLastError();

@@ -898,6 +898,16 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   // of the segment's earlier 32-groups (agg2) and of the earlier CTAs of
   // this CTA's group (agg)
   const uint32_t sz = tid < nr ? sizes[r0 + tid] : 0u;
+  // the first 512 bytes of this warp's first U tiles' slots do not depend on
+  // the scan: load them now, in flight together with the sizes and counters
+  constexpr int U = 8;
+  const uint8_t* const sl0 = slots + r0 * (uint64_t)TILE_SLOT;
+  uint4 v[U];
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const int i = warp + u * NWG;
+    v[u] = i < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane) : make_uint4(0, 0, 0, 0);
+  }
   const uint64_t g2lo = glo >> 5, g2 = c >> 5;
   unsigned long long part = (uint64_t)tid < (c & 31) ? ws->agg[(c & ~31ull) + tid] : 0u;
   {
@@ -961,26 +971,41 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   }
   __syncthreads();
   // ---- copy: warp w moves tiles w, w+NWG, ... (U of them per batch, all
-  // loads in flight).  Lane l holds 16-byte source chunk l of a 31-chunk
+  // loads in flight, the first batch's issued before the scan).  Lane l
+  // holds 16-byte source chunk l of a 31-chunk
   // window of the tile's slot (aligned); aligned destination chunk k is
   // funnel-shifted from chunks k and k+1 (shuffled from lane k+1); the
   // ragged head/tail bytes (shared with the neighbouring tiles' chunks) are
   // stored byte-wise.
   if (nr > 0) {
     uint8_t* const base = S.blob + HEADER_BYTES + excl;
-    const uint8_t* const sl0 = slots + r0 * (uint64_t)TILE_SLOT;
-    constexpr int U = 8;
     long long cka = 0, ckb = 0, ckc = 0;
     for (int i0 = warp; i0 < nr; i0 += NWG * U) {
       if (i0 == warp) cka = clock64();
-      uint4 v[U];
       int len[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int i = i0 + u * NWG;
         len[u] = i < nr ? (int)(s_loc[i + 1] - s_loc[i]) : 0;
-        v[u] = 16 * lane < len[u] + 16 ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane)
-                                       : make_uint4(0, 0, 0, 0);
+        if (i0 != warp)
+          v[u] = i < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane)
+                        : make_uint4(0, 0, 0, 0);
+      }
+      // ragged head/tail bytes of every tile first (one round trip for the
+      // batch; non-coherent loads, so they are not ordered behind the stores)
+      uint32_t hb[U], tb[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int i = i0 + u * NWG;
+        hb[u] = tb[u] = 0;
+        if (len[u] == 0) continue;
+        const uint8_t* src = sl0 + (uint64_t)i * TILE_SLOT;
+        const uint8_t* dst = base + s_loc[i];
+        const int L = len[u];
+        const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+        const int t0 = h + 16 * ((L - h) >> 4);
+        if (lane < h) hb[u] = __ldg(src + lane);
+        if (lane >= 16 && lane - 16 < L - t0) tb[u] = __ldg(src + t0 + lane - 16);
       }
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -1019,8 +1044,8 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
           }
         }
         const int t0 = h + 16 * nfull;  // tail bytes [t0, L)
-        if (lane < h) dst[lane] = src[lane];
-        if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = src[t0 + lane - 16];
+        if (lane < h) dst[lane] = (uint8_t)hb[u];
+        if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = (uint8_t)tb[u];
         if (i0 == warp && u == 0) ckb = clock64();
       }
       if (i0 == warp) ckc = clock64();
