@@ -64,13 +64,17 @@ struct DecodeArgs {
   Status* st;
 };
 
-// Fused step: the received tile's bytes are staged synchronously (one
-// staging buffer per warp keeps 16 warps resident; measured faster than two
-// asynchronous stagings with 13 warps).
+// Fused step: the received tile's bytes are staged synchronously and the
+// local values are loaded for the current tile only (one value buffer, one
+// staging buffer per warp): 24 warps per SM hide the latency better than
+// 16 double-buffered or 13 fully asynchronous warps (measured).
 constexpr bool STEP_ASYNC_STAGE = false;
-constexpr int ENC_WARP_SMEM = 2 * TILE_VALUES * 4 + (STEP_ASYNC_STAGE ? 2 : 1) * STAGE_BYTES;
+constexpr int STEP_BUFS = 1;
+constexpr int ENC_WARP_SMEM = STEP_BUFS * TILE_VALUES * 4 + (STEP_ASYNC_STAGE ? 2 : 1) * STAGE_BYTES;
 // warps per encoder CTA (one CTA per SM): as many as shared memory allows
-__host__ __device__ constexpr int enc_warps(int src) { return src == 1 ? (STEP_ASYNC_STAGE ? 13 : 16) : 24; }
+__host__ __device__ constexpr int enc_warps(int src) {
+  return src == 1 ? (STEP_ASYNC_STAGE ? 13 : (STEP_BUFS == 2 ? 16 : 24)) : 24;
+}
 constexpr int DEC_WARP_SMEM = TILE_VALUES * 4 + 2 * STAGE_BYTES;  // value tile + two stagings
 
 // -------------------------------------------------------------------------
@@ -767,9 +771,10 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   constexpr int WSMEM = SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4;
   unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
-  float* xsb1 = reinterpret_cast<float*>(my + TILE_VALUES * 4);
-  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4);  // fused step only
-  uint32_t* stg1 = STEP_ASYNC_STAGE ? reinterpret_cast<uint32_t*>(my + 2 * TILE_VALUES * 4 + STAGE_BYTES) : stg0;
+  constexpr bool ONEBUF = SRC == SRC_STEP && STEP_BUFS == 1;
+  float* xsb1 = ONEBUF ? xsb0 : reinterpret_cast<float*>(my + TILE_VALUES * 4);
+  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + (ONEBUF ? 1 : 2) * TILE_VALUES * 4);  // fused step only
+  uint32_t* stg1 = STEP_ASYNC_STAGE ? stg0 + STAGE_WORDS : stg0;
   const int wi = SRC == SRC_STEP ? warp : 0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
   __syncthreads();
@@ -804,21 +809,29 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   unsigned int j1 = j < total ? claim() : total;
   InTile in_cur{0, 0, 0}, in_nxt{0, 0, 0};
   if (STEP_ASYNC_STAGE) in_cur = stage_in(j, stg0);
-  if (j < total) prefetch_tile(a, j, xsb0, lane, pol_in);
+  if (j < total && !ONEBUF) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
   unsigned long long wait_ns = 0, ndone = 0;
   uint32_t dummy = 0;
   while (j < total) {
-    if (STEP_ASYNC_STAGE) in_nxt = stage_in(j1, buf ? stg0 : stg1);
-    prefetch_tile(a, j1, buf ? xsb0 : xsb1, lane, pol_in);
     const unsigned long long tw0 = a.dbg ? gtimer() : 0;
-    cp_async_wait_1();
-    __syncwarp();
-    if (a.dbg) wait_ns += gtimer() - tw0;
-    if (SRC == SRC_STEP && !STEP_ASYNC_STAGE) {
+    if (ONEBUF) {
+      // values of this tile (cp.async) and its received bytes (loads) together
+      prefetch_tile(a, j, xsb0, lane, pol_in);
       in_cur = stage_in(j, stg0);
+      cp_async_wait_all();
       __syncwarp();
+    } else {
+      if (STEP_ASYNC_STAGE) in_nxt = stage_in(j1, buf ? stg0 : stg1);
+      prefetch_tile(a, j1, buf ? xsb0 : xsb1, lane, pol_in);
+      cp_async_wait_1();
+      __syncwarp();
+      if (SRC == SRC_STEP && !STEP_ASYNC_STAGE) {
+        in_cur = stage_in(j, stg0);
+        __syncwarp();
+      }
     }
+    if (a.dbg) wait_ns += gtimer() - tw0;
     const int k = NSEG > 1 ? seg_of_tile(a, j) : 0;
     const Seg& S = a.seg[k];
     const SegGeom G = seg_geom(S.n);
