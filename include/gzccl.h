@@ -50,7 +50,7 @@ typedef struct gz_status {
 uint64_t gz_compress_bound(uint64_t n);
 uint64_t gz_num_tiles(uint64_t n);        /* tiles of GZ_TILE_BLOCKS blocks */
 uint32_t gz_tile_blocks(void);            /* 32-value blocks per tile (CTA) */
-uint64_t gz_sidecar_bytes(uint64_t n);    /* u64 tile offsets + u16 group offsets */
+uint64_t gz_sidecar_bytes(uint64_t n);    /* u64 tile offsets [tiles+1] + u8 block widths [tiles*32] */
 uint64_t gz_workspace_bytes(uint64_t n);  /* CTA status words, per-tile offsets and the L2 scratch */
 
 /* ---- setup ---------------------------------------------------------------- */
@@ -61,7 +61,7 @@ int gz_status_reset(gz_status* d_status, gz_stream_t stream);
  * gz_compress replaces codec.compress(data, eb, workspace) (codec.py:149-270).
  *   x[n] f32 -> blob (reference byte format, header included) of length
  *   *d_len; blob_cap >= gz_compress_bound(n); blob 16-byte aligned.
- *   sidecar (gz_sidecar_bytes, may be NULL): tile/group offsets for decoders.
+ *   sidecar (gz_sidecar_bytes, may be NULL): tile offsets and block widths for decoders.
  *   d_block_offsets (nb = ceil(n/32) u64, may be NULL): payload offset of
  *   every block == np.cumsum(sizes) exclusive scan (codec.py:241-243).
  *   block must be 32.

@@ -54,16 +54,18 @@ QParams make_qparams(double eb) {
   return p;
 }
 
+// Sidecar: u64 payload offset of every tile [ntiles + 1], then the width
+// byte of every block, a full tile of 32 per tile [ntiles * 32].
 struct SidecarView {
   uint64_t* tile_off;
-  uint16_t* sub_off;
+  uint8_t* widths;
 };
 SidecarView sidecar_view(const void* sc, uint64_t n) {
   SidecarView v{nullptr, nullptr};
   if (!sc) return v;
   const uint64_t nt = ntiles_of(n);
   v.tile_off = reinterpret_cast<uint64_t*>(const_cast<void*>(sc));
-  v.sub_off = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(const_cast<void*>(sc)) + 8 * (nt + 1));
+  v.widths = reinterpret_cast<uint8_t*>(const_cast<void*>(sc)) + 8 * (nt + 1);
   return v;
 }
 
@@ -274,7 +276,7 @@ uint64_t gz_num_tiles(uint64_t n) { return ntiles_of(n); }
 uint32_t gz_tile_blocks(void) { return TB; }
 uint64_t gz_sidecar_bytes(uint64_t n) {
   const uint64_t nt = ntiles_of(n);
-  return ((8 * (nt + 1) + 2 * nt * GROUPS) + 15) & ~15ull;
+  return ((8 * (nt + 1) + (uint64_t)TB * nt) + 15) & ~15ull;
 }
 uint64_t gz_workspace_bytes(uint64_t n) { return ws_bytes_for_tiles(ntiles_of(n)); }
 
@@ -299,7 +301,7 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.sub_off, 0, 0, 0, 0};
+  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.widths, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
@@ -321,7 +323,7 @@ int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, 
   SidecarView sv = sidecar_view(sidecar, n);
   a.blob = blob;
   a.tile_off = sv.tile_off;
-  a.sub_off = sv.sub_off;
+  a.widths = sv.widths;
   a.n = n;
   a.tw = 2.0 * eb;
   a.y = y;
@@ -373,7 +375,8 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   iw.cbase = reinterpret_cast<unsigned long long*>(take(nch * 8));
   // a block has at least 5 bytes: more blocks than that cannot be walked
   const uint64_t nb_eff = std::min<uint64_t>(nblocks(n), payload_len / 5 + 2);
-  iw.g8 = reinterpret_cast<unsigned long long*>(take(((nb_eff + GROUP - 1) / GROUP) * 8));
+  iw.gt = reinterpret_cast<unsigned long long*>(take(((nb_eff + TB - 1) / TB) * 8));
+  iw.widths = sidecar_view(sidecar, n).widths;
   const uint8_t* payload = blob + HEADER_BYTES;
   count_launch(4);  // idx_segments, idx_chunks, idx_resolve, idx_emit
   idx_segments<<<(unsigned)nseg, 160, 0, s>>>(payload, payload_len, iw);
@@ -388,10 +391,10 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   idx_emit<<<(unsigned)nch, CH, 0, s>>>(payload, payload_len, nseg, n, iw, st);
   if (nblocks(n) > payload_len / 5 + 1) return (int)cudaGetLastError();  // certainly truncated: no sidecar
   const uint64_t nt = ntiles_of(n);
-  const uint64_t work = std::max<uint64_t>(nt * GROUPS, nt + 1);
+  const uint64_t work = nt + 1;
   SidecarView sv = sidecar_view(sidecar, n);
   count_launch();
-  idx_sidecar<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(iw, n, payload_len, sv.tile_off, sv.sub_off);
+  idx_sidecar<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(iw, n, payload_len, sv.tile_off);
   return (int)cudaGetLastError();
 }
 
@@ -407,7 +410,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView so = sidecar_view(sidecar_out, m);
-  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.sub_off, 0, 0, 0, 0};
+  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   const WsView wv = carve(ws, ntiles_of(m));
@@ -418,7 +421,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   SidecarView si = sidecar_view(sidecar_in, m);
   a.in_blob = blob_in;
   a.in_tile_off = si.tile_off;
-  a.in_sub_off = si.sub_off;
+  a.in_w = si.widths;
   a.in_tw = 2.0 * eb;
   a.op = op;
   a.acc_out = acc_out;
@@ -458,7 +461,7 @@ int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg
       const uint64_t n = h_counts[i];
       SidecarView sv{nullptr, nullptr};
       if (sidecars) sv = sidecar_view(reinterpret_cast<uint8_t*>(sidecars) + h_seg_sidecar_off[i], n);
-      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.sub_off, 0, 0, 0, tiles};
+      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.widths, 0, 0, 0, tiles};
       tiles += ntiles_of(n);
       xoff += n;
     }

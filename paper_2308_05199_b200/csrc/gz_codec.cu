@@ -23,7 +23,7 @@ struct Seg {
   uint8_t* blob;           // header at 0, payload at 24; 16-byte aligned (may be a peer pointer)
   uint64_t* out_len;       // 24 + payload bytes
   uint64_t* out_tile_off;  // sidecar: [ntiles + 1] payload offsets of tiles
-  uint16_t* out_sub_off;   // sidecar: [ntiles * GROUPS] offsets of every 8th block inside its tile
+  uint8_t* out_w;          // sidecar: [ntiles * TB] width byte of every block (0..32 or 255)
   uint64_t cta_base;       // first encoder CTA of this segment
   uint64_t gcta_base;      // first gather CTA of this segment (a multiple of 32)
   uint64_t gcta_n;         // gather CTAs of this segment (up to the next base: padding)
@@ -48,7 +48,7 @@ struct EncodeArgs {
   // fused step only (NSEG == 1)
   const uint8_t* in_blob;  // received blob (header + payload)
   const uint64_t* in_tile_off;
-  const uint16_t* in_sub_off;
+  const uint8_t* in_w;
   double in_tw;
   int op;
   float* acc_out;          // optional: reduced values (f32)
@@ -57,7 +57,7 @@ struct EncodeArgs {
 struct DecodeArgs {
   const uint8_t* blob;     // header + payload (may be a peer pointer)
   const uint64_t* tile_off;
-  const uint16_t* sub_off;
+  const uint8_t* widths;
   uint64_t n;
   double tw;
   float* y;
@@ -176,43 +176,43 @@ __device__ __forceinline__ void init_step_table(double* s_step, double tw) {
 }
 
 // -------------------------------------------------------------------------
-// Block starts of a staged compressed tile.  The sidecar gives the offset of
-// every 8th block; lane g < 4 walks 8 width bytes (codec.py:305-320) and
-// records starts and widths in the warp's shared arrays.  Caller __syncwarp()s.
-// `sub` = this lane's sidecar sub-offset (lanes < GROUPS); all lanes call.
-__device__ __forceinline__ void walk_groups(const uint32_t* stage, int base, int tile_bytes, int sub, int nblk,
-                                            uint64_t b0, uint64_t nb, int last_cnt, Status* st, uint16_t* s_start,
-                                            uint8_t* s_w, int lane) {
-  const int g = lane;
-  const int sub_next = __shfl_down_sync(0xFFFFFFFFu, sub, 1);
-  if (g >= GROUPS || g * GROUP >= nblk) return;
-  const int g0 = g * GROUP;
-  const int gblk = min(GROUP, nblk - g0);
-  const int gend = (g0 + GROUP < nblk) ? sub_next : tile_bytes;
-  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(stage) + base;
-  int pos = sub;
-  for (int k = 0; k < gblk; ++k) {
-    const int w = bytes[pos];
-    const uint64_t gb = b0 + g0 + k;
-    const int cnt = (gb == nb - 1) ? last_cnt : 32;
-    int size;
+// Block start of this lane's block inside a staged compressed tile: the
+// sidecar carries every block's width byte, so the block sizes of
+// codec.py:309-316 and their exclusive scan give all 32 starts at once (one
+// warp scan instead of the reference's sequential walk, codec.py:305-320).
+// The sidecar is cross-checked against the staged bytes (width byte at each
+// start, total = tile size).  Returns -1 for lanes without a (valid) block.
+__device__ __forceinline__ int block_start(const uint32_t* stage, int base, int tile_bytes, int w, int nblk,
+                                           uint64_t b0, uint64_t nb, int last_cnt, Status* st, int lane) {
+  const bool active = lane < nblk;
+  const uint64_t gb = b0 + lane;
+  const int cnt = (gb == nb - 1) ? last_cnt : 32;
+  int size = 0;
+  bool bad = false;
+  if (active) {
     if (w == RAW_WIDTH) size = 1 + 4 * cnt;
     else if (w <= 32) size = 5 + ((cnt - 1) * w + 7) / 8;
-    else {
-      record_decode_error(st, gb, DE_WIDTH, w);
-      for (int r = k; r < gblk; ++r) s_start[g0 + r] = 0xFFFF;
-      return;
-    }
-    s_start[g0 + k] = (uint16_t)pos;
-    s_w[g0 + k] = (uint8_t)w;
-    pos += size;
-    if (pos > gend) {
-      record_decode_error(st, gb, DE_SIDECAR);
-      for (int r = k + 1; r < gblk; ++r) s_start[g0 + r] = 0xFFFF;
-      return;
-    }
+    else bad = true;
   }
-  if (pos != gend) record_decode_error(st, b0 + g0 + gblk - 1, DE_SIDECAR);
+  int incl = size;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  const int start = incl - size;
+  if (!active) return -1;
+  if (bad) {
+    record_decode_error(st, gb, DE_WIDTH, w);
+    return -1;
+  }
+  const uint8_t* bytes = reinterpret_cast<const uint8_t*>(stage) + base;
+  if (total != tile_bytes || bytes[start] != w) {
+    record_decode_error(st, gb, DE_SIDECAR);
+    return -1;
+  }
+  return start;
 }
 
 // Values of one block (codec.py:331-369) from its staged bytes.
@@ -269,18 +269,18 @@ __device__ __forceinline__ void decode_values(const uint32_t* stage, int base, i
   }
 }
 
-// Decode this lane's block (walked by walk_groups) into its xs row.
+// Decode this lane's block (start from block_start) into its xs row.
 // MODE 0: xs = decoded.  MODE 1: xs = op(xs, decoded), collectives.py:32-39.
 template <int MODE>
-__device__ __forceinline__ void decode_row(const uint32_t* stage, int base, int nblk, uint64_t b0, uint64_t nb,
-                                           int last_cnt, double tw, float* xs, int op, const double* s_step,
-                                           const uint16_t* s_start, const uint8_t* s_w, int lane) {
+__device__ __forceinline__ void decode_row(const uint32_t* stage, int base, int my_start, int my_w, uint64_t b0,
+                                           uint64_t nb, int last_cnt, double tw, float* xs, int op, const double* s_step,
+                                           int lane) {
   const int row = lane;
-  if (row >= nblk || s_start[row] == 0xFFFF) return;
+  if (my_start < 0) return;
   const uint64_t gb = b0 + row;
   const int cnt = (gb == nb - 1) ? last_cnt : 32;
   float out[32];
-  decode_values(stage, base, s_start[row], s_w[row], cnt, tw, s_step, out);
+  decode_values(stage, base, my_start, my_w, cnt, tw, s_step, out);
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
     float4* dst = reinterpret_cast<float4*>(xs + xs_index(row, c));
@@ -450,12 +450,12 @@ __device__ __forceinline__ void prefetch_tile(const EncodeArgs<NSEG>& a, uint64_
 template <int SRC, int NSEG>
 __device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg& S, uint64_t v0, int cnt,
                                            const uint32_t* stage, int base, double tw, const double* s_step,
-                                           const uint16_t* s_start, const uint8_t* s_w, int lane, float* row) {
+                                           int my_start, int my_w, int lane, float* row) {
   const float* src = S.x + v0 + (uint64_t)lane * 32;
   for (int j = 0; j < 32; ++j) row[j] = j < cnt ? src[j] : 0.0f;
   if (SRC == SRC_STEP) {
     float dec[32];
-    decode_values(stage, base, s_start[lane], s_w[lane], cnt, tw, s_step, dec);
+    decode_values(stage, base, my_start, my_w, cnt, tw, s_step, dec);
     for (int j = 0; j < cnt; ++j) row[j] = a.op == OP_SUM ? __fadd_rn(row[j], dec[j]) : np_maximum(row[j], dec[j]);
   }
 }
@@ -467,21 +467,21 @@ __device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg&
 template <int SRC, int NSEG, bool FAST>
 __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
                                            float* xs, uint32_t* dst, int pos0, bool run_mode, uint32_t& carry,
-                                           uint32_t* stage, int in_base, int in_bytes, int in_sub, uint16_t* s_start,
-                                           uint8_t* s_w, const double* s_step, uint64_t pol_keep, int lane) {
+                                           uint32_t* stage, int in_base, int in_bytes, int in_w,
+                                           const double* s_step, uint64_t pol_keep, int lane) {
   const uint64_t nb = G.nb, b0 = tile * TB, v0 = b0 * BLOCK;
   const int last_cnt = G.last_cnt;
   const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
   const int nval = (int)(G.n - v0 < (uint64_t)TILE_VALUES ? G.n - v0 : (uint64_t)TILE_VALUES);
-  int base = 0;
+  int base = 0, in_start = -1;
 
   // ---- 1. fused step: combine the received blob's tile into xs
   // (its compressed bytes were staged asynchronously with the local values)
   if (SRC == SRC_STEP) {
     base = in_base;
-    walk_groups(stage, base, in_bytes, in_sub, nblk, b0, nb, last_cnt, a.st, s_start, s_w, lane);
+    in_start = block_start(stage, base, in_bytes, in_w, nblk, b0, nb, last_cnt, a.st, lane);
     __syncwarp();
-    decode_row<1>(stage, base, nblk, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, s_start, s_w, lane);
+    decode_row<1>(stage, base, in_start, in_w, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, lane);
     __syncwarp();
     if (a.acc_out) drain_values(xs, a.acc_out, v0, nval, lane);
     __syncwarp();
@@ -499,7 +499,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
     if (FAST && cnt == 32) fb = fast_block(xs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
     if (fb == FB_SLOW) {  // rare: exact replay of the whole block
       float row[32];
-      if (FAST && cnt == 32) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, s_start, s_w, lane, row);
+      if (FAST && cnt == 32) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
       else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
       x0 = row[0];
       uint32_t zl[32];
@@ -546,7 +546,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
     ap.pol = pol_keep;
     if (raw) {
       float row[32];
-      reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, s_start, s_w, lane, row);
+      reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
       ap.append(255ull | ((uint64_t)__float_as_uint(x0) << 8), 5);
       int j = 1;
       for (; j + 1 < cnt; j += 2)
@@ -597,9 +597,8 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
     else my_carry = ap.pend;  // the run's next tile completes this word
   }
   carry = __shfl_sync(0xFFFFFFFFu, my_carry, nblk > 0 ? nblk - 1 : 0);
-  // sub-offsets (final values, independent of the tile's position)
-  const int st8 = __shfl_sync(0xFFFFFFFFu, start, (lane & 3) * GROUP);
-  if (lane < GROUPS && S.out_sub_off) S.out_sub_off[tile * GROUPS + lane] = (uint16_t)(lane * GROUP < nblk ? st8 : tile_bytes);
+  // block widths (the sidecar; independent of the tile's position)
+  if (active && S.out_w) S.out_w[b0 + lane] = (uint8_t)wbyte;
   if (active && a.blk_off) a.blk_off[b0 + lane] = (unsigned long long)start;  // made absolute in phase B
   return tile_bytes;
 }
@@ -762,8 +761,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   constexpr int NW = enc_warps(SRC);
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
-  __shared__ uint16_t s_start[SRC == SRC_STEP ? NW : 1][TB];
-  __shared__ uint8_t s_w[SRC == SRC_STEP ? NW : 1][TB];
   // the gather kernel may be scheduled as soon as SMs free up; it waits for
   // this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -775,7 +772,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   float* xsb1 = ONEBUF ? xsb0 : reinterpret_cast<float*>(my + TILE_VALUES * 4);
   uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + (ONEBUF ? 1 : 2) * TILE_VALUES * 4);  // fused step only
   uint32_t* stg1 = STEP_ASYNC_STAGE ? stg0 + STAGE_WORDS : stg0;
-  const int wi = SRC == SRC_STEP ? warp : 0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
   __syncthreads();
   const uint64_t c = blockIdx.x;
@@ -793,7 +789,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   // fused step: the received blob's tile jn is staged with the local values
   // (same cp.async group); its offsets come from the sidecar
   struct InTile {
-    int base, bytes, sub;
+    int base, bytes, w;
   };
   auto stage_in = [&](unsigned int jn, uint32_t* stg) {
     InTile r{0, 0, 0};
@@ -801,7 +797,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
       const uint64_t ts = a.in_tile_off[jn], te = a.in_tile_off[jn + 1];
       r.base = stage_bytes<STEP_ASYNC_STAGE>(stg, a.in_blob + HEADER_BYTES, ts, te, lane);
       r.bytes = (int)(te - ts);
-      r.sub = lane < GROUPS ? (int)a.in_sub_off[(uint64_t)jn * GROUPS + lane] : 0;
+      r.w = a.in_w[(uint64_t)jn * TB + lane];  // (the sidecar has a full tile of widths)
     }
     return r;
   };
@@ -840,7 +836,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
                                                 reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), 0,
                                                 false, dummy, (STEP_ASYNC_STAGE && buf) ? stg1 : stg0, in_cur.base,
                                                 in_cur.bytes,
-                                                in_cur.sub, s_start[wi], s_w[wi], s_step, pol_keep, lane);
+                                                in_cur.w, s_step, pol_keep, lane);
     if (lane == 0) {
       a.tile_rel[j] = (uint32_t)tb;
       const uint64_t g = S.gcta_base + (t >> a.gshift);
@@ -1094,8 +1090,6 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
 __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[256];
-  __shared__ uint16_t s_start[WARPS][TB];
-  __shared__ uint8_t s_w[WARPS][TB];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   unsigned char* my = smem + warp * DEC_WARP_SMEM;
   float* xs = reinterpret_cast<float*>(my);
@@ -1136,10 +1130,9 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
     const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
     const uint64_t v0 = b0 * BLOCK;
     const int nval = (int)(n - v0 < (uint64_t)TILE_VALUES ? n - v0 : (uint64_t)TILE_VALUES);
-    walk_groups(stage, base, (int)(te - ts), lane < GROUPS ? (int)a.sub_off[t * GROUPS + lane] : 0, nblk, b0, nb,
-                last_cnt, a.st, s_start[warp], s_w[warp], lane);
-    __syncwarp();
-    decode_row<0>(stage, base, nblk, b0, nb, last_cnt, a.tw, xs, 0, s_step, s_start[warp], s_w[warp], lane);
+    const int w = lane < nblk ? (int)a.widths[t * TB + lane] : 0;
+    const int start = block_start(stage, base, (int)(te - ts), w, nblk, b0, nb, last_cnt, a.st, lane);
+    decode_row<0>(stage, base, start, w, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
     drain_values(xs, a.y, v0, nval, lane);
     __syncwarp();

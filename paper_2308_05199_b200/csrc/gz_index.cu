@@ -33,7 +33,8 @@ struct IndexWs {
   unsigned* ccount;       // [nchunk][NE]
   long long* centry;      // [nchunk] actual entry (offset in first segment), <0 if unreachable
   unsigned long long* cbase;  // [nchunk] block index of the first start in the chunk
-  unsigned long long* g8;     // [ceil(nb/8)] payload offset of block 8k
+  unsigned long long* gt;     // [ceil(nb/32)] payload offset of block 32k (tile starts)
+  uint8_t* widths;            // sidecar width byte of every block (may be null)
 };
 
 __device__ __forceinline__ int full_size(int w) { return w == RAW_WIDTH ? 1 + 4 * BLOCK : 5 + (31 * w + 7) / 8; }
@@ -160,7 +161,8 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
       idx_error(st, blk, w, DE_WIDTH);
       return;
     }
-    if ((blk & (GROUP - 1)) == 0) ws.g8[blk / GROUP] = pos;
+    if ((blk & (TB - 1)) == 0) ws.gt[blk / TB] = pos;
+    if (ws.widths) ws.widths[blk] = (uint8_t)w;
     pos += size;
     if (pos > psize) {  // 319-320
       idx_error(st, blk, 0, DE_TRUNC);
@@ -177,19 +179,12 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
   if (blk < nb && pos >= psize && pos < send) idx_error(st, blk, 0, DE_TRUNC);
 }
 
-__global__ void idx_sidecar(const IndexWs ws, uint64_t n, uint64_t psize, uint64_t* tile_off, uint16_t* sub_off) {
+__global__ void idx_sidecar(const IndexWs ws, uint64_t n, uint64_t psize, uint64_t* tile_off) {
   const uint64_t nb = (n + BLOCK - 1) / BLOCK;
   const uint64_t ntiles = (nb + TB - 1) / TB;
-  const uint64_t ng = (nb + GROUP - 1) / GROUP;
   const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i < ntiles) tile_off[i] = ws.g8[i * GROUPS];
+  if (i < ntiles) tile_off[i] = ws.gt[i];
   if (i == ntiles) tile_off[ntiles] = psize;
-  if (i < ntiles * GROUPS) {
-    const uint64_t t = i / GROUPS;
-    // groups past the last block point at the end of the tile
-    const uint64_t tend = (t + 1 < ntiles) ? ws.g8[(t + 1) * GROUPS] : psize;
-    sub_off[i] = (uint16_t)((i < ng ? ws.g8[i] : tend) - ws.g8[t * GROUPS]);
-  }
 }
 
 }  // namespace gz
