@@ -134,22 +134,18 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   }
   a.nctas = base;
   a.total_tiles = total_tiles;
-  // tiles per gather CTA: 32, doubled until the grid fits MAXGRID; each
-  // segment's gather CTAs start at a multiple of 32 (agg2 groups)
-  uint32_t gs = 5;
-  auto gctas = [&](uint32_t sh) {
+  // tiles per gather group (one warp each): 8, doubled until the groups fit
+  // MAXGRID
+  uint32_t gs = 3;
+  auto ngroups = [&](uint32_t sh) {
     uint64_t g = 0;
-    for (int k = 0; k < a.nseg; ++k) {
-      g = (g + 31) & ~31ull;
-      g += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << sh) - 1) >> sh);
-    }
+    for (int k = 0; k < a.nseg; ++k) g += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << sh) - 1) >> sh);
     return g;
   };
-  while (gctas(gs) > (uint64_t)MAXGRID && (1u << gs) < (uint32_t)GATHER_THREADS) ++gs;
-  if (gctas(gs) > (uint64_t)MAXGRID) return GZ_EINVAL;
+  while (ngroups(gs) > (uint64_t)MAXGRID && gs < 10) ++gs;
+  if (ngroups(gs) > (uint64_t)MAXGRID) return GZ_EINVAL;
   uint64_t gbase = 0;
   for (int k = 0; k < a.nseg; ++k) {
-    gbase = (gbase + 31) & ~31ull;
     a.seg[k].gcta_base = gbase;
     a.seg[k].gcta_n = std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << gs) - 1) >> gs);
     gbase += a.seg[k].gcta_n;
@@ -162,8 +158,17 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   if (rc) return rc;
   if (g_dbg_flags & 1) return 0;
   // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
+  static int gcap = -1;
+  if (gcap < 0) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<NSEG>, GATHER_THREADS, 0);
+    gcap = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
+  }
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)gbase);
+  cfg.gridDim = dim3((unsigned)std::min<uint64_t>((gbase + GATHER_THREADS / 32 - 1) / (GATHER_THREADS / 32),
+                                                  (uint64_t)gcap));
   cfg.blockDim = dim3(GATHER_THREADS);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = s;

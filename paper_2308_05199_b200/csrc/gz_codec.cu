@@ -25,8 +25,8 @@ struct Seg {
   uint64_t* out_tile_off;  // sidecar: [ntiles + 1] payload offsets of tiles
   uint8_t* out_w;          // sidecar: [ntiles * TB] width byte of every block (0..32 or 255)
   uint64_t cta_base;       // first encoder CTA of this segment
-  uint64_t gcta_base;      // first gather CTA of this segment (a multiple of 32)
-  uint64_t gcta_n;         // gather CTAs of this segment (up to the next base: padding)
+  uint64_t gcta_base;      // first gather group of this segment
+  uint64_t gcta_n;         // gather groups of this segment
   uint64_t tile_base;      // first slot of this segment in tile_rel / scratch
 };
 
@@ -35,8 +35,8 @@ struct EncodeArgs {
   Seg seg[NSEG];
   int nseg;
   uint64_t nctas;          // encoder CTAs (== grid), split over segments by cta_base
-  uint64_t ngctas;         // gather CTAs, 2^gshift tiles each, split by gcta_base
-  uint32_t gshift;         // log2(tiles per gather CTA), 5..7
+  uint64_t ngctas;         // gather groups (one warp each), 2^gshift tiles each, split by gcta_base
+  uint32_t gshift;         // log2(tiles per gather group), 3..10
   uint64_t total_tiles;    // tiles over all segments
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
@@ -842,6 +842,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
       const uint64_t g = S.gcta_base + (t >> a.gshift);
       atomicAdd(&a.ws->agg[g], (unsigned)tb);
       atomicAdd(&a.ws->agg2[g >> 5], (unsigned)tb);
+      atomicAdd(&a.ws->agg3[g >> 10], (unsigned)tb);
     }
     ++ndone;
     __syncwarp();
@@ -860,223 +861,183 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
 }
 
 // Encoder, kernel 2 of 2: the exclusive scan of codec.py:241-243 at tile
-// granularity and the gather of the slots into the blob.  Gather CTA g of a
-// segment owns 2^gshift consecutive tiles.  The encoder has added every
-// tile's size into agg[g] and agg2[g/32], so the CTA's base offset is a
-// parallel sum of at most 32 + MAXGRID/32/GATHER_THREADS*... loads issued
-// together with the load of its tiles' sizes (no look-back, no waiting on
-// other CTAs).  A block scan gives the tile offsets, and every thread then
-// produces aligned 16-byte chunks of the CTA's contiguous output range --
-// possibly in a peer GPU's memory (the NVLink send of a fused reduce-scatter
-// step) -- coalesced, all loads of a thread in flight at once.  Launched as a
-// programmatic dependent of the encoder, so its launch overlaps the encoder's
-// tail.
-constexpr int GATHER_THREADS = 128;
+// granularity and the gather of the slots into the blob.  Gather group g of
+// a segment = 2^gshift consecutive tiles, handled by ONE warp (no CTA
+// barriers; warps stride over the groups).  The encoder has added every
+// tile's size into agg[g], agg2[g/32] and agg3[g/1024], so a group's base
+// offset is a warp-parallel sum of at most 16 + 31 + 31 counters; a warp scan of
+// the sizes gives the tile offsets (the sidecar's tile_off), and the warp
+// moves its tiles as aligned 16-byte chunks into the blob -- possibly in a
+// peer GPU's memory (the NVLink send of a fused reduce-scatter step).  The
+// first batch of slot windows is loaded together with the sizes and
+// counters.  Launched as a programmatic dependent of the encoder, so its
+// launch overlaps the encoder's tail.
+constexpr int GATHER_THREADS = 256;
+constexpr int GATHER_U = 8;  // tiles per batch
+
+// Copy one tile (L bytes at a 128-aligned slot) to dst (any alignment) with
+// the whole warp; `cur` holds slot chunk `lane` (prefetched), hb/tb the
+// ragged head/tail bytes (prefetched).  Aligned destination chunk k is
+// funnel-shifted from source chunks k and k+1 (shuffled from lane k+1).
+__device__ __forceinline__ void gather_tile(uint8_t* dst, const uint8_t* src, int L, uint4 cur, uint32_t hb,
+                                            uint32_t tb, int lane) {
+  const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+  const int wo = h >> 2, sh = (h & 3) * 8;
+  const int nfull = (L - h) >> 4;
+  for (int w0 = 0; w0 < nfull; w0 += 31) {  // 31 output chunks per 32-chunk window
+    if (w0) {
+      const int q = w0 + lane;
+      cur = 16 * q < L + 16 ? *reinterpret_cast<const uint4*>(src + 16 * q) : make_uint4(0, 0, 0, 0);
+    }
+    uint4 nxt;
+    nxt.x = __shfl_down_sync(0xFFFFFFFFu, cur.x, 1);
+    nxt.y = __shfl_down_sync(0xFFFFFFFFu, cur.y, 1);
+    nxt.z = __shfl_down_sync(0xFFFFFFFFu, cur.z, 1);
+    nxt.w = __shfl_down_sync(0xFFFFFFFFu, cur.w, 1);
+    const int kk = w0 + lane;
+    if (lane < 31 && kk < nfull) {
+      const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
+      const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
+      const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
+      const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
+      const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
+      uint4 o;
+      o.x = __funnelshift_r(a0, a1, sh);
+      o.y = __funnelshift_r(a1, a2, sh);
+      o.z = __funnelshift_r(a2, a3, sh);
+      o.w = __funnelshift_r(a3, a4, sh);
+      *reinterpret_cast<uint4*>(dst + h + 16 * kk) = o;
+    }
+  }
+  const int t0 = h + 16 * nfull;  // tail bytes [t0, L)
+  if (lane < h) dst[lane] = (uint8_t)hb;
+  if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = (uint8_t)tb;
+}
 
 template <int NSEG>
 __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG> a) {
-  constexpr int NWG = GATHER_THREADS / 32;
-  __shared__ uint32_t s_wsum[NWG];
-  __shared__ unsigned long long s_red[NWG];
-  __shared__ uint32_t s_loc[GATHER_THREADS + 1];  // local payload offset of each tile, [nr] = total
+  constexpr int U = GATHER_U;
   __shared__ int s_last;
-  const long long ck0 = clock64();
   asm volatile("griddepcontrol.wait;" ::: "memory");  // the encoder grid is complete
-  const long long ck1 = clock64();
-  const unsigned long long gt1 = a.dbg ? gtimer() : 0;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, lane = tid & 31;
   TileWs* ws = a.ws;
-  const uint64_t c = blockIdx.x;
-  int k = 0;
-  if (NSEG > 1) {
+  const uint64_t nwarps = (uint64_t)gridDim.x * (GATHER_THREADS / 32);
+  for (uint64_t c = (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (tid >> 5); c < a.ngctas; c += nwarps) {
+    int k = 0;
+    if (NSEG > 1) {
 #pragma unroll 1
-    for (int i = 1; i < a.nseg; ++i)
-      if (a.seg[i].gcta_base <= c) k = i;
-  }
-  const Seg& S = a.seg[k];
-  const uint64_t glo = S.gcta_base;
-  const bool real = c - glo < S.gcta_n;  // padding CTAs only retire
-  const SegGeom G = seg_geom(S.n);
-  const uint64_t r0 = (c - glo) << a.gshift;
-  const uint64_t r1 = real ? umin64(r0 + (1u << a.gshift), G.ntiles) : r0;
-  const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
-  const uint32_t* const sizes = a.tile_rel + S.tile_base;
-  const uint8_t* const slots = a.scratch + S.tile_base * (uint64_t)TILE_SLOT;
+      for (int i = 1; i < a.nseg; ++i)
+        if (a.seg[i].gcta_base <= c) k = i;
+    }
+    const Seg& S = a.seg[k];
+    const uint64_t glo = S.gcta_base;
+    const SegGeom G = seg_geom(S.n);
+    const uint64_t r0 = (c - glo) << a.gshift;
+    const uint64_t r1 = umin64(r0 + (1u << a.gshift), G.ntiles);
+    const int nr = r1 > r0 ? (int)(r1 - r0) : 0;
+    const uint32_t* sizes = a.tile_rel + S.tile_base + r0;
+    const uint8_t* sl0 = a.scratch + (S.tile_base + r0) * (uint64_t)TILE_SLOT;
 
-  // ---- all independent loads first: this CTA's tile sizes, the byte counts
-  // of the segment's earlier 32-groups (agg2) and of the earlier CTAs of
-  // this CTA's group (agg)
-  const uint32_t sz = tid < nr ? sizes[r0 + tid] : 0u;
-  // the first 512 bytes of this warp's first U tiles' slots do not depend on
-  // the scan: load them now, in flight together with the sizes and counters
-  constexpr int U = 8;
-  const uint8_t* const sl0 = slots + r0 * (uint64_t)TILE_SLOT;
-  uint4 v[U];
+    // ---- independent loads first: the first 32 sizes, the first batch of
+    // slot windows, the counters of the segment's earlier groups
+    uint32_t sz = lane < nr ? sizes[lane] : 0u;
+    uint4 v[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int i = warp + u * NWG;
-    v[u] = i < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane) : make_uint4(0, 0, 0, 0);
-  }
-  const uint64_t g2lo = glo >> 5, g2 = c >> 5;
-  unsigned long long part = (uint64_t)tid < (c & 31) ? ws->agg[(c & ~31ull) + tid] : 0u;
-  {
-    uint32_t v[4];
+    for (int u = 0; u < U; ++u)
+      v[u] = u < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)u * TILE_SLOT + 16 * lane) : make_uint4(0, 0, 0, 0);
+    // bytes of the launch's groups before c minus those before the segment's
+    // first group glo: <= 16 + 31 + 31 terms each, one load per lane per level
+    auto prefix_terms = [&](uint64_t x) -> unsigned long long {
+      unsigned long long v = 0;
+      if ((uint64_t)lane < (x >> 10)) v += ws->agg3[lane];
+      if ((uint64_t)lane < ((x >> 5) & 31)) v += ws->agg2[((x >> 10) << 5) + lane];
+      if ((uint64_t)lane < (x & 31)) v += ws->agg[((x >> 5) << 5) + lane];
+      return v;
+    };
+    unsigned long long base = warp_sum_u64(prefix_terms(c) - prefix_terms(glo));  // payload offset of the group
+
+    for (int s0 = 0; s0 < nr; s0 += 32) {  // 32 tiles (one per lane) at a time
+      if (s0) sz = s0 + lane < nr ? sizes[s0 + lane] : 0u;
+      uint32_t incl = sz;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
-      const uint64_t q = g2lo + tid + m * GATHER_THREADS;
-      v[m] = q < g2 ? ws->agg2[q] : 0u;
-    }
-    part += (unsigned long long)v[0] + v[1] + v[2] + v[3];
-  }
-  part = warp_sum_u64(part);
-  // ---- block scan of this CTA's tile sizes
-  uint32_t incl = sz;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, incl, d);
-    if (lane >= d) incl += v;
-  }
-  if (lane == 31) s_wsum[warp] = incl;
-  if (lane == 0) s_red[warp] = part;
-  __syncthreads();
-  const long long ck2 = clock64();
-  // every CTA has read agg/agg2 once it is counted: the last one zeroes them
-  if (tid == 0) s_last = atomicAdd(&ws->done, 1ull) == a.ngctas - 1;
-  uint32_t wpre = 0, agg = 0;
-  unsigned long long excl = 0;
-#pragma unroll
-  for (int w2 = 0; w2 < NWG; ++w2) {
-    wpre += w2 < warp ? s_wsum[w2] : 0u;
-    agg += s_wsum[w2];
-    excl += s_red[w2];
-  }
-  if (tid < nr) {
-    const uint64_t t = r0 + tid;
-    const unsigned long long o = excl + wpre + incl - sz;
-    if (S.out_tile_off) S.out_tile_off[t] = o;
-    if (a.blk_off && k == 0) {
-      const uint64_t bb0 = t * TB, bb1 = umin64(bb0 + TB, G.nb);
-      for (uint64_t b = bb0; b < bb1; ++b) a.blk_off[b] += o;
-    }
-    s_loc[tid] = wpre + incl - sz;
-  }
-  if (tid == 0) s_loc[nr] = agg;
-  if (real && c == glo && tid < 6) {  // codec.py:158, HEADER "<4s4xQd"
-    uint32_t hw;
-    if (tid == 0) hw = 0x31435A47u;  // "GZC1"
-    else if (tid == 1) hw = 0;
-    else if (tid == 2) hw = (uint32_t)G.n;
-    else if (tid == 3) hw = (uint32_t)(G.n >> 32);
-    else {
-      const unsigned long long eb = __double_as_longlong(a.qp.eb);
-      hw = tid == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
-    }
-    reinterpret_cast<uint32_t*>(S.blob)[tid] = hw;
-  }
-  if (real && c == glo + S.gcta_n - 1 && tid == 0) {  // the segment's last CTA knows the total
-    const unsigned long long total = excl + agg;
-    if (S.out_tile_off) S.out_tile_off[G.ntiles] = total;
-    *S.out_len = HEADER_BYTES + total;
-  }
-  __syncthreads();
-  // ---- copy: warp w moves tiles w, w+NWG, ... (U of them per batch, all
-  // loads in flight, the first batch's issued before the scan).  Lane l
-  // holds 16-byte source chunk l of a 31-chunk
-  // window of the tile's slot (aligned); aligned destination chunk k is
-  // funnel-shifted from chunks k and k+1 (shuffled from lane k+1); the
-  // ragged head/tail bytes (shared with the neighbouring tiles' chunks) are
-  // stored byte-wise.
-  if (nr > 0) {
-    uint8_t* const base = S.blob + HEADER_BYTES + excl;
-    long long cka = 0, ckb = 0, ckc = 0;
-    for (int i0 = warp; i0 < nr; i0 += NWG * U) {
-      if (i0 == warp) cka = clock64();
-      int len[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NWG;
-        len[u] = i < nr ? (int)(s_loc[i + 1] - s_loc[i]) : 0;
-        if (i0 != warp)
-          v[u] = i < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane)
-                        : make_uint4(0, 0, 0, 0);
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, d);
+        if (lane >= d) incl += t;
       }
-      // ragged head/tail bytes of every tile first (one round trip for the
-      // batch; non-coherent loads, so they are not ordered behind the stores)
-      uint32_t hb[U], tb[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NWG;
-        hb[u] = tb[u] = 0;
-        if (len[u] == 0) continue;
-        const uint8_t* src = sl0 + (uint64_t)i * TILE_SLOT;
-        const uint8_t* dst = base + s_loc[i];
-        const int L = len[u];
-        const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
-        const int t0 = h + 16 * ((L - h) >> 4);
-        if (lane < h) hb[u] = __ldg(src + lane);
-        if (lane >= 16 && lane - 16 < L - t0) tb[u] = __ldg(src + t0 + lane - 16);
+      const uint32_t loc = incl - sz;  // offset inside this 32-tile run
+      const uint32_t run = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      if (s0 + lane < nr) {
+        const uint64_t t = r0 + s0 + lane;
+        const unsigned long long o = base + loc;
+        if (S.out_tile_off) S.out_tile_off[t] = o;
+        if (a.blk_off && k == 0) {
+          const uint64_t bb0 = t * TB, bb1 = umin64(bb0 + TB, G.nb);
+          for (uint64_t b = bb0; b < bb1; ++b) a.blk_off[b] += o;
+        }
       }
+      const int nrun = min(32, nr - s0);
+      for (int b0 = 0; b0 < nrun; b0 += U) {
+        if (s0 || b0) {
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int i = i0 + u * NWG;
-        if (len[u] == 0) continue;  // warp-uniform
-        const uint8_t* src = sl0 + (uint64_t)i * TILE_SLOT;
-        uint8_t* dst = base + s_loc[i];
-        const int L = len[u];
-        const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
-        const int wo = h >> 2, sh = (h & 3) * 8;
-        const int nfull = (L - h) >> 4;  // aligned destination chunks
-        uint4 cur = v[u];
-        for (int w0 = 0; w0 < nfull; w0 += 31) {  // 31 output chunks per window
-          if (w0) {
-            const int q = w0 + lane;
-            cur = 16 * q < L + 16 ? *reinterpret_cast<const uint4*>(src + 16 * q) : make_uint4(0, 0, 0, 0);
-          }
-          uint4 nxt;
-          nxt.x = __shfl_down_sync(0xFFFFFFFFu, cur.x, 1);
-          nxt.y = __shfl_down_sync(0xFFFFFFFFu, cur.y, 1);
-          nxt.z = __shfl_down_sync(0xFFFFFFFFu, cur.z, 1);
-          nxt.w = __shfl_down_sync(0xFFFFFFFFu, cur.w, 1);
-          const int k = w0 + lane;
-          if (lane < 31 && k < nfull) {
-            const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-            const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-            const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-            const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-            const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-            uint4 o;
-            o.x = __funnelshift_r(a0, a1, sh);
-            o.y = __funnelshift_r(a1, a2, sh);
-            o.z = __funnelshift_r(a2, a3, sh);
-            o.w = __funnelshift_r(a3, a4, sh);
-            *reinterpret_cast<uint4*>(dst + h + 16 * k) = o;
+          for (int u = 0; u < U; ++u) {
+            const int i = s0 + b0 + u;
+            v[u] = b0 + u < nrun ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)i * TILE_SLOT + 16 * lane)
+                                 : make_uint4(0, 0, 0, 0);
           }
         }
-        const int t0 = h + 16 * nfull;  // tail bytes [t0, L)
-        if (lane < h) dst[lane] = (uint8_t)hb[u];
-        if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = (uint8_t)tb[u];
-        if (i0 == warp && u == 0) ckb = clock64();
+        // offsets/sizes of the batch's tiles (from their lanes), then the
+        // ragged head/tail bytes (one round trip for the batch)
+        uint32_t Ls[U], offs[U], hb[U], tb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int src_lane = min(b0 + u, 31);
+          Ls[u] = __shfl_sync(0xFFFFFFFFu, sz, src_lane);
+          offs[u] = __shfl_sync(0xFFFFFFFFu, loc, src_lane);
+          if (b0 + u >= nrun) Ls[u] = 0;
+          hb[u] = tb[u] = 0;
+          if (Ls[u]) {
+            const int L = (int)Ls[u];
+            const uint8_t* src = sl0 + (uint64_t)(s0 + b0 + u) * TILE_SLOT;
+            const uint8_t* dst = S.blob + HEADER_BYTES + base + offs[u];
+            const int h = min(L, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
+            const int t0 = h + 16 * ((L - h) >> 4);
+            if (lane < h) hb[u] = __ldg(src + lane);
+            if (lane >= 16 && lane - 16 < L - t0) tb[u] = __ldg(src + t0 + lane - 16);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (Ls[u])
+            gather_tile(S.blob + HEADER_BYTES + base + offs[u], sl0 + (uint64_t)(s0 + b0 + u) * TILE_SLOT,
+                        (int)Ls[u], v[u], hb[u], tb[u], lane);
       }
-      if (i0 == warp) ckc = clock64();
+      base += run;
     }
-    if (a.dbg && tid == 0) {
-      unsigned long long* d = a.dbg + 4096 * 24 * 12 + 16384 * 8 + c * 4;
-      d[0] = ckb - cka; d[1] = ckc - ckb; d[2] = clock64() - ckc; d[3] = 1;
+    if (c == glo && lane < 6) {  // codec.py:158, HEADER "<4s4xQd"
+      uint32_t hw;
+      if (lane == 0) hw = 0x31435A47u;  // "GZC1"
+      else if (lane == 1) hw = 0;
+      else if (lane == 2) hw = (uint32_t)G.n;
+      else if (lane == 3) hw = (uint32_t)(G.n >> 32);
+      else {
+        const unsigned long long eb = __double_as_longlong(a.qp.eb);
+        hw = lane == 4 ? (uint32_t)eb : (uint32_t)(eb >> 32);
+      }
+      reinterpret_cast<uint32_t*>(S.blob)[lane] = hw;
+    }
+    if (c == glo + S.gcta_n - 1 && lane == 0) {  // the segment's last group knows the total
+      if (S.out_tile_off) S.out_tile_off[G.ntiles] = base;
+      *S.out_len = HEADER_BYTES + base;
     }
   }
-  const long long ck3 = clock64();
-  // ---- the last CTA to be counted zeroes agg/agg2 for the next launch
+  // ---- retire: the last CTA zeroes the counters for the next launch
   __syncthreads();
-  if (a.dbg && tid == 0) {
-    unsigned long long* d = a.dbg + 4096 * 24 * 12 + c * 8;
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    d[0] = gt1; d[1] = ck1 - ck0; d[2] = ck2 - ck1; d[3] = ck3 - ck2; d[4] = clock64() - ck3; d[5] = smid; d[6] = nr;
-    d[7] = gtimer();
-  }
+  if (tid == 0) s_last = atomicAdd(&ws->done, 1ull) == gridDim.x - 1;
+  __syncthreads();
   if (s_last) {
     for (uint64_t g = tid; g < a.ngctas; g += GATHER_THREADS) ws->agg[g] = 0;
     for (uint64_t g = tid; g < (a.ngctas + 31) / 32; g += GATHER_THREADS) ws->agg2[g] = 0;
+    for (uint64_t g = tid; g < (a.ngctas + 1023) / 1024; g += GATHER_THREADS) ws->agg3[g] = 0;
     if (tid == 0) {
       ws->done = 0;
       ws->claim = 0;

@@ -49,11 +49,12 @@ constexpr int MAGIC32_BITS = 0x4B400000;
 
 // ---- device workspace: zero-initialised once, reused by every launch -------
 // Layout: this header, tile sizes (u32 per tile), scratch slots.
-// agg[g] = compressed bytes of gather CTA g's tiles and agg2[g / 32] = bytes
-// of gather CTAs 32*(g/32) .. +31, accumulated by the encoder kernel and
+// agg[g], agg2[g / 32], agg3[g / 1024] = compressed bytes of gather group g,
+// of groups 32*(g/32) .. +31 and of groups 1024*(g/1024) .. +1023,
+// accumulated by the encoder kernel (over all segments of a launch) and
 // zeroed again by the last gather CTA to retire, so no per-launch memset is
 // needed and CUDA-graph replay is safe.
-constexpr int MAXGRID = 16384;   // gather CTAs per launch (segments 32-aligned)
+constexpr int MAXGRID = 16384;   // gather groups per launch
 constexpr int TILE_SLOT = 4224;  // scratch bytes reserved per tile (>= 32 * 129, 128-aligned)
 struct TileWs {
   unsigned long long done;          // gather retire counter (own 128-byte line)
@@ -62,6 +63,7 @@ struct TileWs {
   unsigned int pad1[31];
   unsigned int agg[MAXGRID];
   unsigned int agg2[MAXGRID / 32];
+  unsigned int agg3[MAXGRID / 1024];
 };
 
 struct Status {                          // error reporting (host-reset to ~0)
