@@ -873,7 +873,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
 // counters.  Launched as a programmatic dependent of the encoder, so its
 // launch overlaps the encoder's tail.
 constexpr int GATHER_THREADS = 256;
-constexpr int GATHER_U = 8;  // tiles per batch
+constexpr int GATHER_U = 4;  // tiles per batch
 
 // Copy one tile (L bytes at a 128-aligned slot) to dst (any alignment) with
 // the whole warp; `cur` holds slot chunk `lane` (prefetched), hb/tb the
