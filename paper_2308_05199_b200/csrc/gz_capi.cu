@@ -22,7 +22,7 @@ constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-paramet
 // benchmark count exactly which launches it timed
 unsigned long long g_launches = 0;
 unsigned long long* g_dbg = nullptr;  // experiments: per-warp timestamps
-int g_dbg_flags = 0;                 // experiments: bit 0 = skip the gather kernel
+int g_dbg_flags = 0;                 // experiments: bit 0 = skip the gather kernel, bit 1 = empty gather
 inline void count_launch(unsigned k = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)k, __ATOMIC_RELAXED); }
 
 inline uint64_t nblocks(uint64_t n) { return (n + BLOCK - 1) / BLOCK; }
@@ -311,6 +311,7 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
   a.dbg = g_dbg;
+  a.dbg_flags = g_dbg_flags;
   const WsView wv = carve(ws, ntiles_of(n));
   a.ws = wv.hdr;
   a.tile_rel = wv.tile_rel;

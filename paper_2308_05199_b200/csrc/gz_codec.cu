@@ -42,6 +42,7 @@ struct EncodeArgs {
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
   TileWs* ws;
   unsigned long long* dbg; // optional per-warp timestamps (experiments)
+  int dbg_flags;           // experiments: bit 1 = gather kernel skips its work
   uint32_t* tile_rel;      // per tile: compressed size (phase A -> phase B)
   uint8_t* scratch;        // per tile one TILE_SLOT-byte slot (16-byte aligned)
   Status* st;
@@ -761,6 +762,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   constexpr int NW = enc_warps(SRC);
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
+  __shared__ unsigned int s_next;
   // the gather kernel may be scheduled as soon as SMs free up; it waits for
   // this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -773,19 +775,30 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + (ONEBUF ? 1 : 2) * TILE_VALUES * 4);  // fused step only
   uint32_t* stg1 = STEP_ASYNC_STAGE ? stg0 + STAGE_WORDS : stg0;
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
+  if (tid == 0) s_next = 0;
   __syncthreads();
   const uint64_t c = blockIdx.x;
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
   const unsigned long long ts0 = a.dbg ? gtimer() : 0;
 
-  // ---- warps claim tiles (over all segments) from one global counter, so
-  // SMs that run faster take more tiles; the next claim is prefetched
+  // ---- tile claiming (over all segments): 7/8 of the tiles are split into
+  // contiguous per-CTA ranges claimed through a shared-memory counter (warps
+  // of one SM do not get equal issue slots); the last 1/8 is claimed from one
+  // global counter, so SMs that run faster take more of the tail.  The next
+  // claim is always one tile ahead (prefetch).
+  const unsigned int total = (unsigned int)a.total_tiles;
+  const unsigned int stat = total - (total >> 3);
+  const unsigned int r0 = (unsigned int)(((uint64_t)stat * c) / gridDim.x);
+  const unsigned int nr = (unsigned int)(((uint64_t)stat * (c + 1)) / gridDim.x) - r0;
+  const unsigned s_next_addr = (unsigned)__cvta_generic_to_shared(&s_next);
   auto claim = [&]() -> unsigned int {
     unsigned int v = 0;
-    if (lane == 0) v = atomicAdd(&a.ws->claim, 1u);
+    if (lane == 0) {
+      asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(v) : "r"(s_next_addr) : "memory");
+      v = v < nr ? r0 + v : stat + atomicAdd(&a.ws->claim, 1u);
+    }
     return __shfl_sync(0xFFFFFFFFu, v, 0);
   };
-  const unsigned int total = (unsigned int)a.total_tiles;
   // fused step: the received blob's tile jn is staged with the local values
   // (same cp.async group); its offsets come from the sidecar
   struct InTile {
@@ -922,7 +935,8 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   const int tid = threadIdx.x, lane = tid & 31;
   TileWs* ws = a.ws;
   const uint64_t nwarps = (uint64_t)gridDim.x * (GATHER_THREADS / 32);
-  for (uint64_t c = (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (tid >> 5); c < a.ngctas; c += nwarps) {
+  const uint64_t cend = (a.dbg_flags & 2) ? 0 : a.ngctas;
+  for (uint64_t c = (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (tid >> 5); c < cend; c += nwarps) {
     int k = 0;
     if (NSEG > 1) {
 #pragma unroll 1

@@ -1,4 +1,4 @@
-"""K1 alone vs K1+K2 (experiment hook gz_debug_set_flags)."""
+"""Compress timing: full, empty gather (launch + retire only), no gather."""
 import sys, os, ctypes
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np, torch
@@ -18,7 +18,7 @@ s = torch.cuda.current_stream().cuda_stream
 def comp():
     lib.gz_compress(x.data_ptr(), n, 1e-4, 32, out.data_ptr(), cap, ws.len_ptr(), sc.data_ptr(), None, tws.data_ptr(), tws.numel(), ws.status_ptr(), s)
 res = {}
-for flags in (0, 1):
+for flags in (0, 2, 0, 2):
     lib.gz_debug_set_flags(flags)
     ts = []
     for it in range(23):
@@ -28,5 +28,4 @@ for flags in (0, 1):
         if it >= 3: ts.append(a.elapsed_time(b) * 1e3)
     res[flags] = float(np.median(ts))
 lib.gz_debug_set_flags(0)
-# the skipped gathers left agg[] non-zero: one full run resets nothing, so rebuild the workspace
-print(f"n={n}: K1+K2 {res[0]:.1f} us, K1 alone {res[1]:.1f} us, K2 share {res[0]-res[1]:.1f} us")
+print(f"n={n}: full {res[0]:.1f} us, empty gather {res[2]:.1f} us -> gather work {res[0]-res[2]:.1f} us")
