@@ -429,12 +429,17 @@ __device__ __forceinline__ void prefetch_tile(const EncodeArgs<NSEG>& a, uint64_
     const int nval = (int)umin64(S.n - v0, TILE_VALUES);
     const float* p = S.x + v0;
     if (nval == TILE_VALUES && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-      const float4* p4 = reinterpret_cast<const float4*>(p);
+      // chunk i = lane + 32j goes to row (lane >> 3) + 4j, 16-byte column
+      // (lane & 7) ^ (row & 7): two swizzle patterns (even / odd j)
+      const float4* p4 = reinterpret_cast<const float4*>(p) + lane;
+      const unsigned sx = (unsigned)__cvta_generic_to_shared(xs) + (lane >> 3) * 128;
+      const unsigned se = sx + ((((lane & 7) ^ (lane >> 3))) << 4);
+      const unsigned so = sx + ((((lane & 7) ^ ((lane >> 3) + 4))) << 4);
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int i = lane + 32 * j;
-        cp_async16_hint(xs + xs_index(i >> 3, i & 7), p4 + i, pol);
-      }
+      for (int j = 0; j < 8; ++j)
+        asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"((j & 1 ? so : se) + 512 * j),
+                     "l"(p4 + 32 * j), "l"(pol)
+                     : "memory");
     } else {
       for (int i = lane; i < TILE_VALUES; i += 32) {
         const float v = i < nval ? __ldcs(p + i) : 0.0f;
@@ -823,7 +828,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   unsigned long long wait_ns = 0, ndone = 0;
   uint32_t dummy = 0;
   while (j < total) {
-    const unsigned long long tw0 = a.dbg ? gtimer() : 0;
     if (ONEBUF) {
       // values of this tile (cp.async) and its received bytes (loads) together
       prefetch_tile(a, j, xsb0, lane, pol_in);
@@ -840,7 +844,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
         __syncwarp();
       }
     }
-    if (a.dbg) wait_ns += gtimer() - tw0;
     const int k = NSEG > 1 ? seg_of_tile(a, j) : 0;
     const Seg& S = a.seg[k];
     const SegGeom G = seg_geom(S.n);
