@@ -559,39 +559,10 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
         ap.append((uint64_t)__float_as_uint(row[j]) | ((uint64_t)__float_as_uint(row[j + 1]) << 32), 8);
       if (j < cnt) ap.append((uint64_t)__float_as_uint(row[j]), 4);
     } else {
-      const uint64_t hdr = (uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8);
-      uint32_t z[31];
-      if (w > 0) load_codes(xs, lane, z);
-      const bool merged = w > 0 && w <= 4 && ncodes == 31;
-      if (merged) {
-        // 8 codes = w bytes ("oct"); with w <= 4 two octs share one append,
-        // with w <= 3 the header takes the first oct along (3 appends/block)
-        const uint32_t P1 = 1u << w, P2 = 1u << (2 * w), P4 = 1u << (4 * w);
-        uint32_t oct[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          uint32_t pr[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            const int j0 = 8 * g + 2 * i;
-            pr[i] = (j0 + 1 < 31) ? z[j0] + z[j0 + 1] * P1 : z[j0];
-          }
-          oct[g] = (pr[0] + pr[1] * P2) + (pr[2] + pr[3] * P2) * P4;
-        }
-        const int L3 = ((ncodes * w + 7) >> 3) - 3 * w;  // bytes of the last oct
-        if (w <= 3) {
-          ap.append(hdr | ((uint64_t)oct[0] << 40), 5 + w);
-          ap.append((uint64_t)oct[1] | ((uint64_t)oct[2] << (8 * w)), 2 * w);
-          if (L3 > 0) ap.append((uint64_t)oct[3], L3);
-        } else {
-          ap.append(hdr, 5);
-          ap.append((uint64_t)oct[0] | ((uint64_t)oct[1] << 32), 8);
-          ap.append((uint64_t)oct[2] | ((uint64_t)oct[3] << 32), 4 + L3);
-        }
-      } else {
-        ap.append(hdr, 5);
-      }
-      if (w > 0 && !merged) {
+      ap.append((uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8), 5);
+      if (w > 0) {
+        uint32_t z[31];
+        load_codes(xs, lane, z);
         if (w <= 8) {
           const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
           const int CB = (ncodes * w + 7) >> 3;
@@ -821,6 +792,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   // global counter, so SMs that run faster take more of the tail.  The next
   // claim is always one tile ahead (prefetch).
   const unsigned int total = (unsigned int)a.total_tiles;
+  // (the fused step's tiles take twice as long: it claims every tile globally)
   const unsigned int stat = total - (total >> 3);
   const unsigned int r0 = (unsigned int)(((uint64_t)stat * c) / gridDim.x);
   const unsigned int nr = (unsigned int)(((uint64_t)stat * (c + 1)) / gridDim.x) - r0;

@@ -7,6 +7,8 @@ sys.path.insert(0, os.path.abspath(os.path.join(os.path.dirname(__file__), "..")
 import numpy as np
 import torch
 
+import paper_2308_05199_b200._lib as _L0
+if os.environ.get("GZ_LIB"): _L0.LIB_PATH = os.environ["GZ_LIB"]
 import paper_2308_05199_b200 as gz
 from oracle import oracle as O
 from paper_2308_05199_b200 import _lib as L
