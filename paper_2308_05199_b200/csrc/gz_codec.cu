@@ -1083,25 +1083,35 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
   const uint8_t* payload = a.blob + HEADER_BYTES;
   const uint64_t stride = (uint64_t)gridDim.x * WARPS;
   uint64_t t = (uint64_t)blockIdx.x * WARPS + warp;
+  // software pipeline: tile t's bytes and widths are staged one iteration
+  // ahead, tile offsets two iterations ahead (they address the staging)
   int buf = 0;
-  uint64_t ts = 0, te = 0;
-  int base = 0;
+  uint64_t ts = 0, te = 0, tsn = 0, ten = 0;
+  int base = 0, w = 0;
   if (t < ntiles) {
     ts = a.tile_off[t];
     te = a.tile_off[t + 1];
     base = stage_bytes<true>(stg0, payload, ts, te, lane);
+    w = a.widths[t * TB + lane];
   }
   cp_async_commit();
+  if (t + stride < ntiles) {
+    tsn = a.tile_off[t + stride];
+    ten = a.tile_off[t + stride + 1];
+  }
   for (; t < ntiles; t += stride) {
-    const uint64_t tn = t + stride;
-    uint64_t tsn = 0, ten = 0;
-    int basen = 0;
+    const uint64_t tn = t + stride, tnn = tn + stride;
+    int basen = 0, wn = 0;
     if (tn < ntiles) {
-      tsn = a.tile_off[tn];
-      ten = a.tile_off[tn + 1];
       basen = stage_bytes<true>(buf ? stg0 : stg1, payload, tsn, ten, lane);
+      wn = a.widths[tn * TB + lane];
     }
     cp_async_commit();
+    uint64_t tsnn = 0, tenn = 0;
+    if (tnn < ntiles) {
+      tsnn = a.tile_off[tnn];
+      tenn = a.tile_off[tnn + 1];
+    }
     cp_async_wait_1();
     __syncwarp();
     uint32_t* stage = buf ? stg1 : stg0;
@@ -1109,9 +1119,9 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
     const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
     const uint64_t v0 = b0 * BLOCK;
     const int nval = (int)(n - v0 < (uint64_t)TILE_VALUES ? n - v0 : (uint64_t)TILE_VALUES);
-    const int w = lane < nblk ? (int)a.widths[t * TB + lane] : 0;
-    const int start = block_start(stage, base, (int)(te - ts), w, nblk, b0, nb, last_cnt, a.st, lane);
-    decode_row<0>(stage, base, start, w, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
+    const int wl = lane < nblk ? w : 0;
+    const int start = block_start(stage, base, (int)(te - ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
+    decode_row<0>(stage, base, start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
     drain_values(xs, a.y, v0, nval, lane);
     __syncwarp();
@@ -1119,6 +1129,9 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
     ts = tsn;
     te = ten;
     base = basen;
+    w = wn;
+    tsn = tsnn;
+    ten = tenn;
   }
 }
 
