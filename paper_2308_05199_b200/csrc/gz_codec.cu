@@ -820,19 +820,39 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     }
     return r;
   };
+  // fused step, one buffer: the received tile's sidecar entries (offsets,
+  // widths) are loaded one tile ahead; its bytes and the local values are
+  // fetched together (one cp.async group) when the tile starts
+  struct InMeta {
+    uint64_t ts, te;
+    int w;
+  };
+  auto load_meta = [&](unsigned int jn) {
+    InMeta m{0, 0, 0};
+    if (SRC == SRC_STEP && jn < total) {
+      m.ts = a.in_tile_off[jn];
+      m.te = a.in_tile_off[jn + 1];
+      m.w = a.in_w[(uint64_t)jn * TB + lane];
+    }
+    return m;
+  };
   unsigned int j = claim();
   unsigned int j1 = j < total ? claim() : total;
   InTile in_cur{0, 0, 0}, in_nxt{0, 0, 0};
+  InMeta m_cur = ONEBUF ? load_meta(j) : InMeta{0, 0, 0};
   if (STEP_ASYNC_STAGE) in_cur = stage_in(j, stg0);
   if (j < total && !ONEBUF) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
   unsigned long long wait_ns = 0, ndone = 0;
   uint32_t dummy = 0;
   while (j < total) {
+    InMeta m_nxt{0, 0, 0};
     if (ONEBUF) {
-      // values of this tile (cp.async) and its received bytes (loads) together
-      prefetch_tile(a, j, xsb0, lane, pol_in);
-      in_cur = stage_in(j, stg0);
+      m_nxt = load_meta(j1);
+      in_cur.base = stage_bytes<true>(stg0, a.in_blob + HEADER_BYTES, m_cur.ts, m_cur.te, lane);
+      in_cur.bytes = (int)(m_cur.te - m_cur.ts);
+      in_cur.w = m_cur.w;
+      prefetch_tile(a, j, xsb0, lane, pol_in);  // commits the group
       cp_async_wait_all();
       __syncwarp();
     } else {
@@ -866,6 +886,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     buf ^= 1;
     j = j1;
     in_cur = in_nxt;
+    m_cur = m_nxt;
     j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
