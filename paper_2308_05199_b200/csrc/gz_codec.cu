@@ -494,7 +494,11 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   }
 
   // ---- 2. closed-loop quantisation, one lane per 32-value block; the codes
-  // replace the values in the lane's shared-memory row
+  // replace the values in the lane's shared-memory row -- except in the fused
+  // step, whose consumed staging buffer takes them, so that the rare raw or
+  // unproven block still finds its values (local + received) in xs
+  __syncwarp();
+  float* zs = SRC == SRC_STEP ? reinterpret_cast<float*>(stage) : xs;
   const bool active = lane < nblk;
   const int cnt = active ? ((b0 + lane == nb - 1) ? last_cnt : 32) : 0;
   uint32_t zor = 0;
@@ -502,15 +506,15 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   float x0 = 0.0f;
   if (active) {
     int fb = FB_SLOW;
-    if (FAST && cnt == 32) fb = fast_block(xs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
+    if (FAST && cnt == 32) fb = fast_block(xs, zs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
     if (fb == FB_SLOW) {  // rare: exact replay of the whole block
       float row[32];
-      if (FAST && cnt == 32) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
+      if (FAST && cnt == 32 && zs == xs) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
       else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
       x0 = row[0];
       uint32_t zl[32];
       zor = slow_block(row, cnt, a.qp, zl, &flags);
-      store_codes(xs, lane, x0, zl);
+      store_codes(zs, lane, x0, zl);
       if (flags & 4) {  // codec.py:83-85: report the first non-finite offset
         for (int j = 0; j < cnt; ++j)
           if (!isfinite(row[j])) {
@@ -552,7 +556,8 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
     ap.pol = pol_keep;
     if (raw) {
       float row[32];
-      reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
+      if (zs == xs) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
+      else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
       ap.append(255ull | ((uint64_t)__float_as_uint(x0) << 8), 5);
       int j = 1;
       for (; j + 1 < cnt; j += 2)
@@ -562,7 +567,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
       ap.append((uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8), 5);
       if (w > 0) {
         uint32_t z[31];
-        load_codes(xs, lane, z);
+        load_codes(zs, lane, z);
         if (w <= 8) {
           const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
           const int CB = (ncodes * w + 7) >> 3;

@@ -201,10 +201,11 @@ __device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, c
 //   maximum inside [elo, ehi] is undecided.
 enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
 
-__device__ __forceinline__ int fast_block(float* xs, int row, double tw, float rtw, float thr, float elo, float ehi,
-                                          uint32_t& zor_out, float& x0) {
-  // The codes overwrite the consumed values in place: slot j of the row
-  // receives code j-1 (slot 0 keeps x0), one 16-byte store per 4 steps.
+__device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, double tw, float rtw, float thr,
+                                          float elo, float ehi, uint32_t& zor_out, float& x0) {
+  // The codes go to the same row of zs (zs == xs: they overwrite the
+  // consumed values in place): slot j of the row receives code j-1 (slot 0
+  // keeps x0), one 16-byte store per 4 steps.
   float4 c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, 0));
   float prev32 = c4.x;
   x0 = c4.x;
@@ -234,7 +235,7 @@ __device__ __forceinline__ int fast_block(float* xs, int row, double tw, float r
     zor |= z;
     zc[j & 3] = z;
     if ((j & 3) == 3)
-      *reinterpret_cast<uint4*>(xs + xs_index(row, j >> 2)) = make_uint4(zc[0], zc[1], zc[2], zc[3]);
+      *reinterpret_cast<uint4*>(zs + xs_index(row, j >> 2)) = make_uint4(zc[0], zc[1], zc[2], zc[3]);
   }
   zor_out = zor;
   const int w = 32 - __clz(zor);

@@ -71,6 +71,22 @@ def timeit(fn, reps=15):
     return float(np.median(ts))
 
 
+class _CI(__import__("ctypes").Structure):
+    _fields_ = [("src", __import__("ctypes").c_void_p), ("dst", __import__("ctypes").c_void_p),
+                ("d_len", __import__("ctypes").c_void_p), ("max_bytes", __import__("ctypes").c_uint64)]
+
+
+def copy(src_where, dst_where):
+    sb, _, sl = B[src_where]
+    db, _, _ = B2[dst_where]
+    it = (_CI * 1)(_CI(sb.data_ptr(), db.data_ptr(), sl.data_ptr(), cap))
+    L.check(lib.gz_copy_items(it, 1, s), "copy")
+
+
+def ce_copy(src_where, dst_where, nbytes):
+    B2[dst_where][0][:nbytes].copy_(B[src_where][0][:nbytes], non_blocking=True)
+
+
 comp("local"), comp("peer")
 torch.cuda.synchronize(d0)
 torch.cuda.synchronize(d1)
@@ -79,7 +95,10 @@ print(f"n=2^{n.bit_length() - 1} blob {L_} B CR {4 * n / L_:.3f}")
 for name, fn in (("compress -> local", lambda: comp("local")), ("compress -> peer", lambda: comp("peer")),
                  ("decode local", lambda: dec("local")), ("decode peer blob", lambda: dec("peer")),
                  ("step local->local", lambda: step("local", "local")), ("step local->peer", lambda: step("local", "peer")),
-                 ("step peer->local", lambda: step("peer", "local"))):
+                 ("step peer->local", lambda: step("peer", "local")),
+                 ("copy kernel peer->local", lambda: copy("peer", "local")),
+                 ("copy kernel local->peer", lambda: copy("local", "peer")),
+                 ("CE copy peer->local", lambda: ce_copy("peer", "local", L_))):
     print(f"{name:22s} {timeit(fn):8.1f} us")
 assert bytes(B["local"][0][:L_].cpu().numpy()) == bytes(B["peer"][0][:L_].cpu().numpy())
 assert bytes(B2["local"][0][:64].cpu().numpy()) == bytes(B2["peer"][0][:64].cpu().numpy())
