@@ -75,6 +75,11 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
  * blob header's values; y[n] f32 output. */
 int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, double eb, float* y,
                           gz_status* d_status, gz_stream_t stream);
+/* y = op(local, decompress(blob)) -- the last step of a standalone
+ * ring_reduce_scatter_c (collectives.py:274-290: decode, then _apply_op with
+ * the local chunk first) without re-compressing the result. */
+int gz_decompress_reduce(const uint8_t* blob, const void* sidecar, const float* local, uint64_t n, double eb, int op,
+                         float* y, gz_status* d_status, gz_stream_t stream);
 
 /* gz_index replaces the sequential block walk of codec.decompress
  * (codec.py:298-322): validates the payload of a blob of header count n and

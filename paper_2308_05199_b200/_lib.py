@@ -30,6 +30,7 @@ SIGNATURES = {
     "gz_status_reset": (i32, [p, p]),
     "gz_compress": (i32, [p, u64, dbl, u32, p, u64, p, p, p, p, u64, p, p]),
     "gz_decompress_sidecar": (i32, [p, p, u64, dbl, p, p, p]),
+    "gz_decompress_reduce": (i32, [p, p, p, u64, dbl, i32, p, p, p]),
     "gz_index": (i32, [p, u64, u64, p, p, u64, p, p]),
     "gz_index_workspace_bytes": (u64, [u64]),
     "gz_reduce_step": (i32, [p, p, p, u64, dbl, i32, p, p, u64, p, p, p, u64, p, p]),

@@ -104,13 +104,12 @@ class Communicator:
         self.copy_stream = torch.cuda.Stream(self.device)  # allgather pulls
 
     # ------------------------------------------------------------------ setup
-    def _setup(self, n: int):
-        if self._n == n:
+    def _setup(self, m_max: int):
+        """(Re)build the IPC buffer for chunks of up to m_max values."""
+        if self._n is not None and self._n >= m_max:
             return
         self._close()
         lib = L.lib()
-        spans = chunk_spans(n, self.world)
-        m_max = max(hi - lo for lo, hi in spans) if spans else 0
         self.layout = _Layout(self.world, m_max)
         self._buf = torch.zeros(self.layout.total, dtype=torch.uint8, device=self.device)
         torch.cuda.synchronize(self.device)
@@ -128,9 +127,8 @@ class Communicator:
                 L.check(lib.gz_ipc_open_handle(ctypes.create_string_buffer(hb, hsz), ctypes.byref(ptr)),
                         "gz_ipc_open_handle")
                 self._peer.append(ptr.value)
-        self._n = n
+        self._n = m_max
         self.epoch = 0
-        self.spans = spans
         dist.barrier(group=self.group)
 
     def _close(self):
@@ -175,34 +173,82 @@ class Communicator:
             ev.record(self.stream)
             self.events.append((label, ev))
 
-    # ------------------------------------------------------------ allreduce
+    # ------------------------------------------------------------ collectives
     def ring_allreduce(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
         """Per-rank ring_allreduce_c (collectives.py:294-308) on this GPU.
 
         Returns this rank's output: its own reduced chunk (i+1) mod N exact, all
         other chunks decoded from their owners' compress-once blobs.
         """
-        ebf = _check_eb(eb)
-        opc = _check_op(op)
-        if x.dim() != 1 or x.dtype != torch.float32 or not x.is_cuda:
-            raise ValueError("expected a flat 1-D float32 CUDA tensor")
-        x = x.contiguous()
-        n = x.numel()
-        N, i = self.world, self.rank
+        x = self._check_input(x)
         if out is None:
             out = torch.empty_like(x)
+        if self.world == 1:
+            out.copy_(x)
+            return out
+        spans = chunk_spans(x.numel(), self.world)
+        self._ring("allreduce", x, spans, _check_eb(eb), _check_op(op), out)
+        return out
+
+    def ring_reduce_scatter(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
+        """Per-rank ring_reduce_scatter_c (collectives.py:258-291): returns the
+        fully reduced chunk (rank + 1) mod N of chunk_spans(n, N).  The last step
+        decodes and reduces without re-compressing (gz_decompress_reduce)."""
+        x = self._check_input(x)
+        N, i = self.world, self.rank
+        spans = chunk_spans(x.numel(), N)
+        lo, hi = spans[(i + 1) % N]
+        if out is None:
+            out = torch.empty(hi - lo, dtype=torch.float32, device=self.device)
         if N == 1:
             out.copy_(x)
             return out
-        self._setup(n)
+        self._ring("reduce_scatter", x, spans, _check_eb(eb), _check_op(op), out)
+        return out
+
+    def ring_allgather(self, chunk: torch.Tensor, eb: float, out: torch.Tensor | None = None):
+        """Per-rank ring_allgather_c (collectives.py:247-255), allgatherv: every
+        rank contributes a chunk of any length; each rank compresses its chunk
+        once and the others decode those bytes; the own chunk is kept verbatim.
+        Returns the concatenation in rank order."""
+        chunk = self._check_input(chunk)
+        ebf = _check_eb(eb)
+        N = self.world
+        counts = [None] * N
+        dist.all_gather_object(counts, int(chunk.numel()), group=self.group)  # lengths ride in the headers
+        total = sum(counts)
+        if out is None:
+            out = torch.empty(total, dtype=torch.float32, device=self.device)
+        if N == 1:
+            out.copy_(chunk)
+            return out
+        lo = [0]
+        for c in counts:
+            lo.append(lo[-1] + c)
+        spans = [(lo[r], lo[r + 1]) for r in range(N)]
+        self._ring("allgather", chunk, spans, ebf, 0, out)
+        return out
+
+    def _check_input(self, x):
+        if not isinstance(x, torch.Tensor) or x.dim() != 1 or x.dtype != torch.float32 or not x.is_cuda:
+            raise ValueError("expected a flat 1-D float32 CUDA tensor")
+        return x.contiguous()
+
+    def _ring(self, mode: str, x, spans, ebf: float, opc: int, out):
+        """Shared executor.  mode: "allreduce" (RS + compress-once AG),
+        "reduce_scatter" (RS only), "allgather" (compress own chunk + AG).
+        spans: per-chunk [lo, hi) (chunk_spans, or the allgatherv layout)."""
+        N, i = self.world, self.rank
+        m_max = max(hi - lo for lo, hi in spans)
+        self._setup(m_max)
         lib = L.lib()
         lay = self.layout
-        spans = self.spans
         s = self.stream.cuda_stream
         ws = self.ws
-        tws = ws.tile_ws(int(lib.gz_workspace_bytes(max(hi - lo for lo, hi in spans))))
+        tws = ws.tile_ws(int(lib.gz_workspace_bytes(m_max)))
         e = self.epoch + 1
         right, left = (i + 1) % N, (i - 1) % N
+        self.spans = spans
 
         def chunk_ptr(t, c):
             return t.data_ptr() + 4 * spans[c][0]
@@ -214,99 +260,138 @@ class Communicator:
             b, sc = lay.slot_off[k]
             return self._addr(r, b), self._addr(r, sc)
 
+        def wait_own_blob_free():
+            # peers must have consumed our previous own blob
+            if self.epoch:
+                for j in range(N):
+                    if j != i:
+                        self._wait(lay.ag_consumed(j), self.epoch, s)
+
+        def own_ready():
+            for j in range(N):
+                if j != i:
+                    self._signal(j, lay.ag_ready(i), e, s)
+
         launches = 0
         self._mark("start")
-        # the right neighbour must have consumed our previous writes
-        if self.epoch:
-            self._wait(lay.rs_consumed(), self.epoch, s)
-        for p in ring_allreduce_plan(N, i):
-            if isinstance(p, Compress):
-                # step 0: compress the local chunk straight into right's slot 0
-                b, sc = slot(p.dst, p.slot)
-                L.check(lib.gz_compress(chunk_ptr(x, p.chunk), msize(p.chunk), ebf, 32, b, lay.blob_cap,
-                                        self._addr(p.dst, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
-                                        tws.numel(), ws.status_ptr(), s), "gz_compress")
-                launches += 1
-                self._mark("compress")
-                self._signal(p.dst, lay.rs_full(p.slot), e, s)
-            elif isinstance(p, Reduce):
-                # fused decompress(recv) + op + compress; the output stores are the send
-                self._wait(lay.rs_full(p.slot), e, s)
-                inb, insc = slot(i, p.slot)
-                if not p.last:
-                    ob, osc = slot(p.dst, p.slot + 1)
-                    olen = self._addr(p.dst, lay.len_off + 8 * (p.slot + 1))
-                    acc = None
-                else:
-                    # our own blob is read by every peer in the allgather
-                    if self.epoch:
-                        for j in range(N):
-                            if j != i:
-                                self._wait(lay.ag_consumed(j), self.epoch, s)
-                    ob, osc = self._addr(i, lay.own_off[0]), self._addr(i, lay.own_off[1])
-                    olen = self._addr(i, lay.len_off + 8 * N)
-                    acc = chunk_ptr(out, p.chunk)
-                L.check(lib.gz_reduce_step(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc, acc, ob,
-                                           lay.blob_cap, olen, osc, tws.data_ptr(), tws.numel(), ws.status_ptr(), s),
-                        "gz_reduce_step")
-                launches += 1
-                self._mark("reduce_last" if p.last else "reduce")
-                if not p.last:
-                    self._signal(p.dst, lay.rs_full(p.slot + 1), e, s)
-                else:
-                    # the owned blob is ready: tell every peer
-                    for j in range(N):
-                        if j != i:
-                            self._signal(j, lay.ag_ready(i), e, s)
-        # compress-once allgather: a side stream pulls each owner's blob +
-        # sidecar over NVLink into our (now free) reduce-scatter slots with one
-        # bulk copy, and releases the owner; the main stream decodes it from
-        # local HBM as soon as it has landed, while the next copy is in flight
-        gathers = [p for p in ring_allreduce_plan(N, i) if not isinstance(p, (Compress, Reduce))]
-        if len(gathers) == 1:
-            # a single owner leaves nothing to overlap the copy with: decode
-            # straight out of its memory over NVLink
-            p = gathers[0]
-            self._wait(lay.ag_ready(p.owner), e, s)
-            L.check(lib.gz_decompress_sidecar(self._addr(p.owner, lay.own_off[0]), self._addr(p.owner, lay.own_off[1]),
-                                              msize(p.chunk), ebf, chunk_ptr(out, p.chunk), ws.status_ptr(), s),
-                    "gz_decompress_sidecar")
-            launches += 1
-            self._mark("decode")
-            self._signal(p.owner, lay.ag_consumed(i), e, s)
-            gathers = []
-        cs = self.copy_stream.cuda_stream
-        if gathers:
-            rs_done = torch.cuda.Event()
-            rs_done.record(self.stream)
-            self.copy_stream.wait_event(rs_done)
-        landed = []
-        for k, p in enumerate(gathers):
-            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(p.owner)), e), "gz_stream_wait_u32_geq")
-            b, sc = lay.slot_off[k]
-            items = (_CopyItem * 2)(
-                _CopyItem(self._addr(p.owner, lay.own_off[0]), self._addr(i, b),
-                          self._addr(p.owner, lay.len_off + 8 * N), lay.blob_cap),
-                _CopyItem(self._addr(p.owner, lay.own_off[1]), self._addr(i, sc), None,
-                          int(lib.gz_sidecar_bytes(msize(p.chunk)))))
-            L.check(lib.gz_copy_items(items, 2, cs), "gz_copy_items")
-            launches += 1
-            self._signal(p.owner, lay.ag_consumed(i), e, cs)
-            ev = torch.cuda.Event()
-            ev.record(self.copy_stream)
-            landed.append(ev)
-        for k, p in enumerate(gathers):
-            self.stream.wait_event(landed[k])
-            b, sc = lay.slot_off[k]
-            L.check(lib.gz_decompress_sidecar(self._addr(i, b), self._addr(i, sc), msize(p.chunk), ebf,
-                                              chunk_ptr(out, p.chunk), ws.status_ptr(), s), "gz_decompress_sidecar")
-            launches += 1
-            self._mark("decode")
+        if mode in ("allreduce", "reduce_scatter"):
+            # the right neighbour must have consumed our previous writes
+            if self.epoch:
+                self._wait(lay.rs_consumed(), self.epoch, s)
+            for p in ring_allreduce_plan(N, i):
+                if isinstance(p, Compress):
+                    # step 0: compress the local chunk straight into right's slot 0
+                    b, sc = slot(p.dst, p.slot)
+                    L.check(lib.gz_compress(chunk_ptr(x, p.chunk), msize(p.chunk), ebf, 32, b, lay.blob_cap,
+                                            self._addr(p.dst, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
+                                            tws.numel(), ws.status_ptr(), s), "gz_compress")
+                    launches += 2
+                    self._mark("compress")
+                    self._signal(p.dst, lay.rs_full(p.slot), e, s)
+                elif isinstance(p, Reduce):
+                    self._wait(lay.rs_full(p.slot), e, s)
+                    inb, insc = slot(i, p.slot)
+                    if p.last and mode == "reduce_scatter":
+                        # decode + reduce into the owned chunk; nothing to re-compress
+                        L.check(lib.gz_decompress_reduce(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc,
+                                                         out.data_ptr(), ws.status_ptr(), s), "gz_decompress_reduce")
+                        launches += 1
+                        self._mark("reduce_last")
+                        continue
+                    # fused decompress(recv) + op + compress; the output stores are the send
+                    if not p.last:
+                        ob, osc = slot(p.dst, p.slot + 1)
+                        olen = self._addr(p.dst, lay.len_off + 8 * (p.slot + 1))
+                        acc = None
+                    else:
+                        wait_own_blob_free()  # our own blob is read by every peer in the allgather
+                        ob, osc = self._addr(i, lay.own_off[0]), self._addr(i, lay.own_off[1])
+                        olen = self._addr(i, lay.len_off + 8 * N)
+                        acc = chunk_ptr(out, p.chunk)
+                    L.check(lib.gz_reduce_step(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc, acc, ob,
+                                               lay.blob_cap, olen, osc, tws.data_ptr(), tws.numel(), ws.status_ptr(),
+                                               s), "gz_reduce_step")
+                    launches += 2
+                    self._mark("reduce_last" if p.last else "reduce")
+                    if not p.last:
+                        self._signal(p.dst, lay.rs_full(p.slot + 1), e, s)
+                    else:
+                        own_ready()
+        if mode == "allgather":
+            # compress our chunk once into our own blob; the own chunk is kept verbatim
+            wait_own_blob_free()
+            L.check(lib.gz_compress(x.data_ptr(), x.numel(), ebf, 32, self._addr(i, lay.own_off[0]), lay.blob_cap,
+                                    self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1]), None,
+                                    tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_compress")
+            launches += 2
+            self._mark("compress")
+            own_ready()
+            if x.numel():
+                out[spans[i][0]:spans[i][1]].copy_(x)
+        if mode in ("allreduce", "allgather"):
+            # compress-once allgather; owner j's chunk is chunk_of(j)
+            owners = [(i - 1 - k) % N for k in range(N - 1)]  # the order the ring delivers them
+            chunk_of = (lambda j: (j + 1) % N) if mode == "allreduce" else (lambda j: j)
+            launches += self._allgather_pull(owners, chunk_of, chunk_ptr, msize, out, ebf, e)
+        else:
+            # nobody pulled our (absent) own blob this epoch
+            for j in range(N):
+                if j != i:
+                    self._signal(j, lay.ag_consumed(i), e, s)
         # our slots are free again: the left neighbour may write the next call's steps
         self._signal(left, lay.rs_consumed(), e, s)
         self.epoch = e
         self.launches_per_call = launches
-        return out
+
+    def _allgather_pull(self, owners, chunk_of, chunk_ptr, msize, out, ebf, e) -> int:
+        """A side stream pulls each owner's blob + sidecar over NVLink into our
+        (free) reduce-scatter slots with one bulk copy and releases the owner;
+        the main stream decodes it from local HBM as soon as it has landed,
+        while the next copy is in flight.  A single owner (N = 2) is decoded
+        straight out of its memory."""
+        lib = L.lib()
+        lay = self.layout
+        N, i = self.world, self.rank
+        s = self.stream.cuda_stream
+        ws = self.ws
+        launches = 0
+        if len(owners) == 1:
+            j = owners[0]
+            c = chunk_of(j)
+            self._wait(lay.ag_ready(j), e, s)
+            L.check(lib.gz_decompress_sidecar(self._addr(j, lay.own_off[0]), self._addr(j, lay.own_off[1]), msize(c),
+                                              ebf, chunk_ptr(out, c), ws.status_ptr(), s), "gz_decompress_sidecar")
+            self._mark("decode")
+            self._signal(j, lay.ag_consumed(i), e, s)
+            return 1
+        cs = self.copy_stream.cuda_stream
+        rs_done = torch.cuda.Event()
+        rs_done.record(self.stream)
+        self.copy_stream.wait_event(rs_done)
+        landed = []
+        for k, j in enumerate(owners):
+            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(j)), e), "gz_stream_wait_u32_geq")
+            b, sc = lay.slot_off[k]
+            items = (_CopyItem * 2)(
+                _CopyItem(self._addr(j, lay.own_off[0]), self._addr(i, b), self._addr(j, lay.len_off + 8 * N),
+                          lay.blob_cap),
+                _CopyItem(self._addr(j, lay.own_off[1]), self._addr(i, sc), None,
+                          int(lib.gz_sidecar_bytes(msize(chunk_of(j))))))
+            L.check(lib.gz_copy_items(items, 2, cs), "gz_copy_items")
+            launches += 1
+            self._signal(j, lay.ag_consumed(i), e, cs)
+            ev = torch.cuda.Event()
+            ev.record(self.copy_stream)
+            landed.append(ev)
+        for k, j in enumerate(owners):
+            c = chunk_of(j)
+            self.stream.wait_event(landed[k])
+            b, sc = lay.slot_off[k]
+            L.check(lib.gz_decompress_sidecar(self._addr(i, b), self._addr(i, sc), msize(c), ebf, chunk_ptr(out, c),
+                                              ws.status_ptr(), s), "gz_decompress_sidecar")
+            launches += 1
+            self._mark("decode")
+        return launches
 
     def compression_ratio(self) -> float:
         """Compressed size of this rank's owned chunk (last call), as a ratio."""

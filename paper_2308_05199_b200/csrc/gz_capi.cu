@@ -320,12 +320,40 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   return launch_encode<SRC_PLAIN, 1>(a, ntiles_of(n), (cudaStream_t)stream);
 }
 
+int gz_decompress_reduce(const uint8_t* blob, const void* sidecar, const float* local, uint64_t n, double eb, int op,
+                         float* y, gz_status* d_status, gz_stream_t stream) {
+  if (!check_eb(eb)) return GZ_EBOUND;
+  if (op != OP_SUM && op != OP_MAX) return GZ_EINVAL;
+  if (!blob || !sidecar || (!y && n) || (!local && n) || !d_status) return GZ_EINVAL;
+  if (n == 0) return 0;
+  DecodeArgs a;
+  std::memset(&a, 0, sizeof(a));
+  SidecarView sv = sidecar_view(sidecar, n);
+  a.local = local;
+  a.op = op;
+  a.blob = blob;
+  a.tile_off = sv.tile_off;
+  a.widths = sv.widths;
+  a.n = n;
+  a.tw = 2.0 * eb;
+  a.y = y;
+  a.st = reinterpret_cast<Status*>(d_status);
+  static int cap = -1;
+  grid_cap(k_tile_decode, DEC_SMEM_BYTES, cap);
+  const uint64_t want = (ntiles_of(n) + WARPS - 1) / WARPS;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
+  count_launch();
+  k_tile_decode<<<grid, CTA_THREADS, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(a);
+  return (int)cudaGetLastError();
+}
+
 int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, double eb, float* y,
                           gz_status* d_status, gz_stream_t stream) {
   if (!check_eb(eb)) return GZ_EBOUND;
   if (!blob || !sidecar || (!y && n) || !d_status) return GZ_EINVAL;
   if (n == 0) return 0;
   DecodeArgs a;
+  std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
   a.blob = blob;
   a.tile_off = sv.tile_off;

@@ -56,6 +56,8 @@ struct EncodeArgs {
 };
 
 struct DecodeArgs {
+  const float* local;      // optional: y = op(local, decoded) (reduce-scatter's last step)
+  int op;
   const uint8_t* blob;     // header + payload (may be a peer pointer)
   const uint64_t* tile_off;
   const uint8_t* widths;
@@ -149,6 +151,20 @@ __device__ __forceinline__ void drain_values(const float* xs, float* __restrict_
       const int row = i >> 5, col = i & 31;
       __stcs(p + i, xs[xs_index(row, col >> 2) + (col & 3)]);
     }
+  }
+}
+
+__device__ __forceinline__ float np_maximum_f(float a, float b) {  // collectives.py:38
+  return isnan(a) ? a : (a > b ? a : b);
+}
+
+// dst = op(local, decoded) (collectives.py:32-39, local first), coalesced
+__device__ __forceinline__ void drain_values_op(const float* xs, const float* __restrict__ local, int op,
+                                                float* __restrict__ dst, uint64_t v0, int nval, int lane) {
+  for (int i = lane; i < nval; i += 32) {
+    const int row = i >> 5, col = i & 31;
+    const float d = xs[xs_index(row, col >> 2) + (col & 3)], l = __ldcs(local + v0 + i);
+    __stcs(dst + v0 + i, op == 0 ? __fadd_rn(l, d) : np_maximum_f(l, d));
   }
 }
 
@@ -1149,7 +1165,8 @@ __global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs
     const int start = block_start(stage, base, (int)(te - ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
     decode_row<0>(stage, base, start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
-    drain_values(xs, a.y, v0, nval, lane);
+    if (a.local) drain_values_op(xs, a.local, a.op, a.y, v0, nval, lane);
+    else drain_values(xs, a.y, v0, nval, lane);
     __syncwarp();
     buf ^= 1;
     ts = tsn;

@@ -55,6 +55,31 @@ def main():
         if out.cpu().numpy().tobytes() != expect[rank].tobytes():
             failures.append(f"oracle n={n} op={op} eb={eb}")
         checked += 1
+    # standalone reduce-scatter and allgather(v) (collectives.py:247-291), vs the oracle,
+    # interleaved with allreduce calls (shared flags and slots)
+    for n, op, eb in ((1 << 20, "sum", 1e-4), (999_999, "max", 1e-3), (5, "sum", 1e-4)):
+        bufs = [O.smooth_field(n, 0.29 * r) + np.random.default_rng(300 + r).normal(0, 1e-3, n).astype(np.float32)
+                for r in range(world)]
+        expect = O.ring_reduce_scatter(bufs, eb, op)
+        got = c.ring_reduce_scatter(torch.from_numpy(bufs[rank]).to(dev), eb, op)
+        torch.cuda.synchronize()
+        if got.cpu().numpy().tobytes() != np.ascontiguousarray(expect[rank], np.float32).tobytes():
+            failures.append(f"reduce_scatter n={n} op={op}")
+        checked += 1
+        out = c.ring_allreduce(torch.from_numpy(bufs[rank]).to(dev), eb, op)
+        torch.cuda.synchronize()
+        if out.cpu().numpy().tobytes() != O.ring_allreduce(bufs, eb, op)[rank].tobytes():
+            failures.append(f"allreduce after reduce_scatter n={n}")
+        checked += 1
+    for sizes in ([1 << 18] * world, [1000 + 77 * r for r in range(world)], [0] + [4096] * (world - 1)):
+        chunks = [O.smooth_field(sz, 0.5 * r) for r, sz in enumerate(sizes)]
+        expect = O.ring_allgather(chunks, 1e-4)
+        for rep in range(2):
+            got = c.ring_allgather(torch.from_numpy(chunks[rank]).to(dev), 1e-4)
+            torch.cuda.synchronize()
+            if got.cpu().numpy().tobytes() != np.ascontiguousarray(expect[rank], np.float32).tobytes():
+                failures.append(f"allgather sizes={sizes[:3]} rep={rep}")
+            checked += 1
     # binomial scatter: golden cases of this rank count, then seeded cases at every root
     for case in G.scatter_cases():
         if case.N != world:
