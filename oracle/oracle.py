@@ -196,6 +196,68 @@ def ring_allgather(chunks, eb, trace=None, raw=False):
     return [np.concatenate([g[i][c] for c in range(N)]) if N > 1 else owned[i].copy() for i in range(N)]
 
 
+def rd_plan(N: int):
+    """RecursiveDoublingPlan, collectives.py:48-86: (pof2, r, steps, role, remapped, actual)."""
+    pof2 = 1 << (N.bit_length() - 1)
+    r = N - pof2
+    steps = pof2.bit_length() - 1
+
+    def role(i):
+        return ("donor" if i % 2 == 0 else "absorber") if i < 2 * r else "direct"
+
+    def remapped(i):
+        return i // 2 if role(i) == "absorber" else i - r
+
+    def actual(v):
+        return 2 * v + 1 if v < r else v + r
+
+    return pof2, r, steps, role, remapped, actual
+
+
+def rd_allreduce(bufs, eb, op="sum", trace=None, raw=False):
+    """rd_allreduce_c, collectives.py:349-424: donors fold into absorbers,
+    log2(pof2) whole-buffer exchanges (each side keeps op(own, decoded
+    partner)), absorbers send the result back compressed."""
+    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb))
+    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else decompress
+    data = [np.ascontiguousarray(b, "<f4").copy() for b in bufs]
+    N = len(data)
+    if N == 1:
+        return [data[0].copy()]
+    pof2, r, steps, role, remapped, actual = rd_plan(N)
+    donors = [i for i in range(N) if role(i) == "donor"]
+    parts = [i for i in range(N) if role(i) != "donor"]
+    if r:
+        sent = {}
+        for i in donors:  # 381-386
+            sent[i] = enc(data[i])
+            if trace is not None:
+                trace.append(("rd", -1, i, i + 1, sent[i]))
+        for i in range(N):  # 389-397
+            if role(i) == "absorber":
+                data[i] = apply_op(op, data[i], dec(sent[i - 1]))
+    for t in range(steps):  # 399-418
+        sent = {}
+        for i in parts:
+            partner = actual(remapped(i) ^ (1 << t))
+            sent[i] = enc(data[i])
+            if trace is not None:
+                trace.append(("rd", t, i, partner, sent[i]))
+        for i in parts:
+            partner = actual(remapped(i) ^ (1 << t))
+            data[i] = apply_op(op, data[i], dec(sent[partner]))
+    if r:
+        sent = {}
+        for i in range(N):  # 420-427
+            if role(i) == "absorber":
+                sent[i] = enc(data[i])
+                if trace is not None:
+                    trace.append(("rd", steps, i, i - 1, sent[i]))
+        for i in donors:  # 430-435
+            data[i] = dec(sent[i + 1])
+    return data
+
+
 def scatter_children(vr: int, size: int):
     """_scatter_children, collectives.py:449-464."""
     mask = 1

@@ -226,6 +226,121 @@ def ring_allgather_virtual(chunks, eb, ws: Workspace | None = None, trace: Trace
     return [torch.cat([gathered[i][c] for c in range(N)]) for i in range(N)]
 
 
+def decompress_reduce(recv: DeviceBlob, local: torch.Tensor, eb: float, op: str, ws: Workspace, out=None,
+                      stream=None) -> torch.Tensor:
+    """op(local, decompress(recv)) in one kernel (no re-compression)."""
+    m = local.numel()
+    if recv.n != m:
+        raise ValueError(f"reduce shape mismatch: ({m},) vs ({recv.n},)")  # collectives.py:33-34
+    out = torch.empty_like(local) if out is None else out
+    L.check(L.lib().gz_decompress_reduce(recv.data.data_ptr(), recv.sidecar.data_ptr(), local.data_ptr(), m, float(eb),
+                                         _check_op(op), out.data_ptr(), ws.status_ptr(), _stream(stream)),
+            "gz_decompress_reduce")
+    return out
+
+
+def rd_plan(N: int):
+    """RecursiveDoublingPlan (collectives.py:48-86): pof2, r, steps and the
+    role / remapped / actual maps (donors are the even ranks below 2r)."""
+    pof2 = 1 << (N.bit_length() - 1)
+    r = N - pof2
+    steps = pof2.bit_length() - 1
+
+    def role(i):
+        return ("donor" if i % 2 == 0 else "absorber") if i < 2 * r else "direct"
+
+    def remapped(i):
+        if role(i) == "donor":
+            raise ValueError(f"rank {i} is a donor and has no remapped id")
+        return i // 2 if role(i) == "absorber" else i - r
+
+    def actual(v):
+        if not 0 <= v < pof2:
+            raise ValueError(f"remapped id {v} out of range [0, {pof2})")
+        return 2 * v + 1 if v < r else v + r
+
+    return pof2, r, steps, role, remapped, actual
+
+
+def rd_allreduce_virtual(buffers, eb, op="sum", ws: Workspace | None = None, trace: Trace | None = None,
+                         counters: list | None = None) -> list[torch.Tensor]:
+    """rd_allreduce_c (collectives.py:349-424) with N virtual ranks on one GPU.
+
+    Whole-buffer exchanges.  The message a participant sends at step t+1 is
+    compress(data after step t), so every reduction that is followed by a
+    send is one fused kernel compress(op(data, decompress(recv))) that also
+    updates data in place (gz_reduce_step); the last reduction of a rank
+    that sends nothing more is gz_decompress_reduce.
+    """
+    ebf = _check_eb(eb)
+    _check_op(op)
+    ws = ws or Workspace()
+    N = len(buffers)
+    data = _dev_inputs(buffers, N, ws.device)
+    _require_equal(data)
+    _check_finite(data)
+    data = [d.clone() for d in data]
+    if counters is None:
+        counters = [Counters() for _ in range(N)]
+    if N == 1:
+        return data
+    pof2, r, steps, role, remapped, actual = rd_plan(N)
+    donors = [i for i in range(N) if role(i) == "donor"]
+    parts = [i for i in range(N) if role(i) != "donor"]
+
+    def send(i, dst, blob):
+        if trace is not None:
+            trace.add(i, dst, blob)
+        counters[i].n_messages += 1
+        counters[i].bytes_sent += len(blob)
+
+    def comp(i):
+        counters[i].n_compress += 1
+        counters[i].raw_bytes_in += 4 * data[i].numel()
+        return compress(data[i], ebf, ws)
+
+    def fused(i, recv):  # data[i] = op(data[i], dec(recv)); returns compress(data[i])
+        counters[i].n_decompress += 1
+        counters[i].n_compress += 1
+        counters[i].raw_bytes_in += 4 * data[i].numel()
+        return reduce_step(recv, data[i], ebf, op, ws, acc_out=data[i])
+
+    def last(i, recv):  # data[i] = op(data[i], dec(recv))
+        counters[i].n_decompress += 1
+        decompress_reduce(recv, data[i], ebf, op, ws, out=data[i])
+
+    # message each participant sends at the next exchange step
+    nxt = {}
+    if r:
+        dblob = {}
+        for i in donors:  # 381-386
+            dblob[i] = comp(i)
+            send(i, i + 1, dblob[i])
+        for i in parts:  # 389-397: absorbers fold their donor in; the fused kernel also
+            # produces their step-0 message
+            nxt[i] = fused(i, dblob[i - 1]) if role(i) == "absorber" else None
+    for t in range(steps):  # 399-418
+        msg = {}
+        for i in parts:
+            msg[i] = nxt[i] if nxt.get(i) is not None else comp(i)
+            send(i, actual(remapped(i) ^ (1 << t)), msg[i])
+        for i in parts:
+            recv = msg[actual(remapped(i) ^ (1 << t))]
+            more = t + 1 < steps or role(i) == "absorber"
+            if more:
+                nxt[i] = fused(i, recv)
+            else:
+                last(i, recv)
+    if r:
+        for i in parts:  # 420-427: the absorbers' final data, already compressed
+            if role(i) == "absorber":
+                send(i, i - 1, nxt[i])
+        for i in donors:  # 430-435
+            counters[i].n_decompress += 1
+            data[i] = decompress(nxt[i + 1], ws)
+    return data
+
+
 # ---------------------------------------------------------------------------
 # binomial-tree scatter (collectives.py:432-532)
 # ---------------------------------------------------------------------------
@@ -337,6 +452,7 @@ ALGORITHMS = {
     "ring-allgather": "allgather",
     "ring-reduce-scatter": "reduce_scatter",
     "ring-allreduce": "allreduce",
+    "rd-allreduce": "allreduce",
     "binomial-scatter": "scatter",
 }
 
@@ -374,7 +490,9 @@ def run_collective(algorithm: str, inputs, *, ranks: int | None = None, eb: floa
     if N is None or N < 1:
         raise ValueError(f"communicator needs at least 1 rank, got {N}")
     counters = [Counters() for _ in range(N)]
-    if family == "allreduce":
+    if algorithm == "rd-allreduce":
+        out = rd_allreduce_virtual(inputs, eb, reduce_op, ws, trace, counters)
+    elif family == "allreduce":
         out = ring_allreduce_virtual(inputs, eb, reduce_op, ws, trace, counters)
     elif family == "reduce_scatter":
         out = ring_reduce_scatter_virtual(inputs, eb, reduce_op, ws, trace, counters)

@@ -142,6 +142,7 @@ class Communicator:
         self._buf = None
         self._n = None
         _scatter_close(self)
+        _rd_close(self)
 
     def close(self):
         try:
@@ -595,3 +596,154 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
 
 
 Communicator.binomial_scatter = binomial_scatter
+
+
+class _RDLayout:
+    """Recursive doubling: one worst-case slot (blob + sidecar) per message a
+    rank can receive -- 0: the donor's buffer (absorbers), 1..steps: the
+    exchange steps, steps+1: the absorber's final result (donors) -- plus
+    full[k] / consumed[k] flags and the blob lengths."""
+
+    def __init__(self, n: int, steps: int):
+        lib = L.lib()
+        self.K = steps + 2
+        off = _al(4 * 2 * self.K)
+        self.len_off = off
+        off += _al(8 * self.K)
+        self.cap = _al(int(lib.gz_compress_bound(n)))
+        self.scb = int(lib.gz_sidecar_bytes(n))
+        self.slot = []
+        for _ in range(self.K):
+            self.slot.append((off, off + self.cap))
+            off += self.cap + _al(self.scb)
+        self.total = off
+
+    def full(self, k):
+        return 4 * k
+
+    def consumed(self, k):
+        return 4 * (self.K + k)
+
+
+def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
+    """This rank's part of rd_allreduce_c (collectives.py:349-424) over NVLink.
+
+    Whole-buffer exchanges with the partner actual(remapped(i) ^ 2^t); every
+    reduction followed by a send is one fused kernel that updates the buffer
+    in place and stores compress(buffer) straight into the partner's slot;
+    the last reduction of a non-absorber is gz_decompress_reduce.  Donors
+    (even ranks below 2r) fold into their absorber first and receive the
+    result compressed at the end.  Outputs are per rank, bit-exact with the
+    reference.
+    """
+    from .collectives import rd_plan
+
+    x = self._check_input(x)
+    ebf = _check_eb(eb)
+    opc = _check_op(op)
+    N, i = self.world, self.rank
+    if out is None:
+        out = torch.empty_like(x)
+    out.copy_(x)
+    if N == 1:
+        return out
+    n = x.numel()
+    pof2, r, steps, role, remapped, actual = rd_plan(N)
+    if getattr(self, "_rd_key", None) != (n, N):
+        _rd_close(self)
+        self._rd_layout = _RDLayout(n, steps)
+        self._rd_buf = torch.zeros(self._rd_layout.total, dtype=torch.uint8, device=self.device)
+        torch.cuda.synchronize(self.device)
+        self._rd_peer = _open_peers(self, self._rd_buf)
+        self._rd_key = (n, N)
+        self._rd_epoch = 0
+        dist.barrier(group=self.group)
+    lib = L.lib()
+    lay, peer = self._rd_layout, self._rd_peer
+    prev, e = self._rd_epoch, self._rd_epoch + 1
+    s = self.stream.cuda_stream
+    ws = self.ws
+    tws = ws.tile_ws(int(lib.gz_workspace_bytes(n)))
+    K = lay.K
+    launches = 0
+
+    def at(rr, off):
+        return peer[rr] + off
+
+    def wait(off, v):
+        if v > 0:
+            L.check(lib.gz_stream_wait_u32_geq(s, at(i, off), v), "gz_stream_wait_u32_geq")
+
+    def signal(rr, off):
+        L.check(lib.gz_stream_write_u32(s, at(rr, off), e), "gz_stream_write_u32")
+
+    def dest(rr, k):  # blob, length word, sidecar of rank rr's slot k
+        b, sc = lay.slot[k]
+        return at(rr, b), at(rr, lay.len_off + 8 * k), at(rr, sc)
+
+    def compress_to(rr, k):
+        nonlocal launches
+        wait(lay.consumed(k), prev)  # rr consumed what we wrote there last call
+        b, ln, sc = dest(rr, k)
+        L.check(lib.gz_compress(out.data_ptr(), n, ebf, 32, b, lay.cap, ln, sc, None, tws.data_ptr(), tws.numel(),
+                                ws.status_ptr(), s), "gz_compress")
+        launches += 2
+        signal(rr, lay.full(k))
+
+    def fused_to(k_in, rr, k):  # out = op(out, dec(my slot k_in)); compress(out) -> rr's slot k
+        nonlocal launches
+        wait(lay.consumed(k), prev)
+        b, ln, sc = dest(rr, k)
+        ib, _, isc = dest(i, k_in)
+        L.check(lib.gz_reduce_step(ib, isc, out.data_ptr(), n, ebf, opc, out.data_ptr(), b, lay.cap, ln, sc,
+                                   tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_reduce_step")
+        launches += 2
+        signal(rr, lay.full(k))
+
+    if role(i) == "donor":
+        a = i + 1
+        compress_to(a, 0)  # 381-386
+        wait(lay.full(K - 1), e)  # 430-435: the absorber's result
+        b, _, sc = dest(i, K - 1)
+        L.check(lib.gz_decompress_sidecar(b, sc, n, ebf, out.data_ptr(), ws.status_ptr(), s), "gz_decompress_sidecar")
+        launches += 1
+        signal(a, lay.consumed(K - 1))
+    else:
+        part = [actual(remapped(i) ^ (1 << t)) for t in range(steps)]
+        if role(i) == "absorber":
+            wait(lay.full(0), e)  # 389-397, fused with the step-0 compression
+            fused_to(0, part[0], 1)
+            signal(i - 1, lay.consumed(0))
+        else:
+            compress_to(part[0], 1)
+        for t in range(steps):  # 399-418
+            wait(lay.full(t + 1), e)
+            if t + 1 < steps:
+                fused_to(t + 1, part[t + 1], t + 2)
+            elif role(i) == "absorber":
+                fused_to(t + 1, i - 1, K - 1)  # 420-427: the result goes back to the donor
+            else:
+                ib, _, isc = dest(i, t + 1)
+                L.check(lib.gz_decompress_reduce(ib, isc, out.data_ptr(), n, ebf, opc, out.data_ptr(), ws.status_ptr(),
+                                                 s), "gz_decompress_reduce")
+                launches += 1
+            signal(part[t], lay.consumed(t + 1))
+    self._rd_epoch = e
+    self.launches_per_call = launches
+    return out
+
+
+def _rd_close(self):
+    peers = getattr(self, "_rd_peer", None)
+    if peers is not None:
+        lib = L.lib()
+        torch.cuda.synchronize(self.device)
+        for r, p in enumerate(peers):
+            if r != self.rank and p:
+                lib.gz_ipc_close(p)
+    self._rd_peer = None
+    self._rd_buf = None
+    self._rd_key = None
+
+
+Communicator.rd_allreduce = rd_allreduce

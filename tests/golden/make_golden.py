@@ -184,6 +184,26 @@ def ring_cases(codec, collectives, simnet):
             out[pre + "msg_dst"] = np.array([t[1] for t in net.trace], np.int64)
             rows.append((algo, N, n, op, eb))
             k += 1
+    # recursive doubling (collectives.py:349-424), appended so earlier cases keep their seeds
+    rd_cfgs = [(2, 100, "sum", 1e-4), (3, 257, "sum", 1e-4), (4, 1000, "sum", 1e-3), (5, 64, "max", 1e-4),
+               (6, 3000, "sum", 1e-4), (7, 31, "sum", 1e-4), (8, 4099, "sum", 1e-4), (8, 700, "max", 1e-3),
+               (4, 0, "sum", 1e-4), (1, 50, "sum", 1e-4), (3, 20000, "sum", 1e-5)]
+    for N, n, op, eb in rd_cfgs:
+        rng = np.random.default_rng(1000 + k)
+        inputs = [smooth(n, 0.37 * r) + rng.normal(0, 1e-3, n).astype(np.float32) for r in range(N)]
+        net = simnet.Network(simnet.CommunicatorSpec(N), record_payloads=True)
+        outputs, rep = simnet.run_collective(net, "rd-allreduce", inputs, eb=eb, reduce_op=op, compute_accuracy=False)
+        pre = f"c{k}_"
+        out[pre + "meta"] = np.array([N, n, 1 if op == "max" else 0], np.int64)
+        out[pre + "algo"] = np.array("rd-allreduce")
+        out[pre + "eb"] = np.array(eb)
+        pack_list(pre + "in", [np.asarray(a, np.float32) for a in inputs], out)
+        pack_list(pre + "out", [np.asarray(o, np.float32) for o in outputs], out)
+        pack_list(pre + "msg", [np.frombuffer(t[3], np.uint8).copy() for t in net.trace], out)
+        out[pre + "msg_src"] = np.array([t[0] for t in net.trace], np.int64)
+        out[pre + "msg_dst"] = np.array([t[1] for t in net.trace], np.int64)
+        rows.append(("rd-allreduce", N, n, op, eb))
+        k += 1
     out["count"] = np.array(k)
     np.savez_compressed(os.path.join(HERE, "ring_cases.npz"), **out)
     return rows

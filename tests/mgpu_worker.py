@@ -80,6 +80,26 @@ def main():
             if got.cpu().numpy().tobytes() != np.ascontiguousarray(expect[rank], np.float32).tobytes():
                 failures.append(f"allgather sizes={sizes[:3]} rep={rep}")
             checked += 1
+    # recursive-doubling allreduce (collectives.py:349-424): golden cases, then the oracle
+    for case in G.ring_cases():
+        if case.algo != "rd-allreduce" or case.N != world:
+            continue
+        for rep in range(2):
+            got = c.rd_allreduce(torch.from_numpy(np.ascontiguousarray(case.inputs[rank], np.float32)).to(dev), case.eb,
+                                 case.op)
+            torch.cuda.synchronize()
+            if got.cpu().numpy().tobytes() != case.outputs[rank].tobytes():
+                failures.append(f"rd golden N={case.N} n={case.n} op={case.op} rep={rep}")
+            checked += 1
+    for n, op, eb in ((1 << 20, "sum", 1e-4), (333_333, "max", 1e-3), (1 << 22, "sum", 1e-5)):
+        bufs = [O.smooth_field(n, 0.41 * r) + np.random.default_rng(500 + r).normal(0, 1e-3, n).astype(np.float32)
+                for r in range(world)]
+        expect = O.rd_allreduce(bufs, eb, op)
+        got = c.rd_allreduce(torch.from_numpy(bufs[rank]).to(dev), eb, op)
+        torch.cuda.synchronize()
+        if got.cpu().numpy().tobytes() != expect[rank].tobytes():
+            failures.append(f"rd oracle n={n} op={op}")
+        checked += 1
     # binomial scatter: golden cases of this rank count, then seeded cases at every root
     for case in G.scatter_cases():
         if case.N != world:

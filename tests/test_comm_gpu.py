@@ -15,7 +15,7 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 
 
 @pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
-@pytest.mark.parametrize("nproc", sorted({2, min(NGPU, 4), min(NGPU, 8)} - {1}))
+@pytest.mark.parametrize("nproc", sorted({2, min(NGPU, 3), min(NGPU, 4), min(NGPU, 8)} - {1}))
 def test_collectives_multi_gpu(nproc):
     if nproc > NGPU:
         pytest.skip("not enough GPUs")

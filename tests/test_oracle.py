@@ -96,6 +96,8 @@ def test_oracle_ring_matches_reference(case, oracle):
         outs = oracle.ring_allreduce(case.inputs, case.eb, case.op, trace)
     elif case.algo == "ring-reduce-scatter":
         outs = oracle.ring_reduce_scatter(case.inputs, case.eb, case.op, trace)
+    elif case.algo == "rd-allreduce":
+        outs = oracle.rd_allreduce(case.inputs, case.eb, case.op, trace)
     else:
         outs = oracle.ring_allgather(case.inputs, case.eb, trace)
     assert len(outs) == case.N
