@@ -401,7 +401,9 @@ def bench_allreduce(args):
     # configs[2]: binomial-tree compressed Scatter of a 1 GiB root buffer vs NCCL scatter
     ns = (1 << 30) // 4
     root_buf = torch.from_numpy(O.smooth_field(ns, 0.0)).to(dev) if rank == 0 else None
-    sc_out = torch.empty(ns // world, dtype=torch.float32, device=dev)
+    from paper_2308_05199_b200.collectives import chunk_spans as _spans
+    lo_, hi_ = _spans(ns, world)[rank]
+    sc_out = torch.empty(hi_ - lo_, dtype=torch.float32, device=dev)
     for _ in range(3):
         c.binomial_scatter(root_buf, EB, root=0, out=sc_out)
     torch.cuda.synchronize()
@@ -416,7 +418,8 @@ def bench_allreduce(args):
         torch.cuda.synchronize()
         st.append(e0.elapsed_time(e1) * 1e-3)
     scatter_gbs = 4 * ns / _max_over_ranks(sum(st) / len(st), dev) / 1e9
-    parts = list(root_buf.chunk(world)) if rank == 0 else None
+    # (NCCL scatter needs equal parts: the largest multiple of N values)
+    parts = list(root_buf[: (ns // world) * world].chunk(world)) if rank == 0 else None
     ys = torch.empty(ns // world, dtype=torch.float32, device=dev)
     for _ in range(3):
         dist.scatter(ys, parts, src=0)
@@ -433,6 +436,24 @@ def bench_allreduce(args):
         nst.append(e0.elapsed_time(e1) * 1e-3)
     nccl_scatter_gbs = 4 * ns / _max_over_ranks(sum(nst) / len(nst), dev) / 1e9
 
+    # recursive-doubling allreduce (the paper's gZ-Allreduce(ReDoub)) on the same tensors
+    rdo = torch.empty_like(x)
+    for _ in range(3):
+        c.rd_allreduce(x, EB, out=rdo)
+    torch.cuda.synchronize()
+    rt = []
+    for _ in range(max(3, min(args.steps, 10))):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        c.rd_allreduce(x, EB, out=rdo)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rt.append(e0.elapsed_time(e1) * 1e-3)
+    rd_gbs = S_CFG2 / _max_over_ranks(sum(rt) / len(rt), dev) / 1e9
+    del rdo
+
     value = S_CFG2 / t / 1e9
     peak, peak_kind = peaks()
     if rank == 0:
@@ -447,6 +468,7 @@ def bench_allreduce(args):
                        "collective_roofline_gbs": round(900.0 * (cr or 1.0), 1),
                        "collective_roofline_frac": round(value / (900.0 * (cr or 1.0)), 4),
                        "scatter_1GiB_gbs": round(scatter_gbs, 2), "nccl_scatter_1GiB_gbs": round(nccl_scatter_gbs, 2),
+                       "rd_allreduce_gbs": round(rd_gbs, 2),
                        "l2": "inputs (512 MiB) larger than L2"},
             "roofline": {"bound": "hbm", "kernel": "fused RS step = k_tile_encode<STEP> + k_gather",
                          "achieved": round(step_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
