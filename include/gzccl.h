@@ -80,6 +80,12 @@ int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, 
  * the local chunk first) without re-compressing the result. */
 int gz_decompress_reduce(const uint8_t* blob, const void* sidecar, const float* local, uint64_t n, double eb, int op,
                          float* y, gz_status* d_status, gz_stream_t stream);
+/* Decode up to GZ_MAX_DECODE_SEGMENTS blobs (with sidecars; blobs may live in
+ * peer GPUs' memory) in one launch: the compress-once allgather decoding every
+ * owner's blob (collectives.py:238-241).  Empty entries (ns[i] == 0) are skipped. */
+#define GZ_MAX_DECODE_SEGMENTS 8
+int gz_decompress_multi(const uint8_t* const* blobs, const void* const* sidecars, const uint64_t* ns, uint32_t count,
+                        double eb, float* const* ys, int reserve_sms, gz_status* d_status, gz_stream_t stream);
 
 /* gz_index replaces the sequential block walk of codec.decompress
  * (codec.py:298-322): validates the payload of a blob of header count n and
@@ -137,6 +143,9 @@ typedef struct {
 } gz_copy_item;
 #define GZ_MAX_COPY_ITEMS 64
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream);
+/* the same on at most sms_budget SMs (0: all), so that it can run beside a
+ * decoder launched with reserve_sms = sms_budget (allgather pipeline) */
+int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget, gz_stream_t stream);
 
 /* number of kernels this library has launched so far (all entry points) */
 uint64_t gz_launch_count(void);

@@ -31,6 +31,7 @@ SIGNATURES = {
     "gz_compress": (i32, [p, u64, dbl, u32, p, u64, p, p, p, p, u64, p, p]),
     "gz_decompress_sidecar": (i32, [p, p, u64, dbl, p, p, p]),
     "gz_decompress_reduce": (i32, [p, p, p, u64, dbl, i32, p, p, p]),
+    "gz_decompress_multi": (i32, [p, p, p, u32, dbl, p, i32, p, p]),
     "gz_index": (i32, [p, u64, u64, p, p, u64, p, p]),
     "gz_index_workspace_bytes": (u64, [u64]),
     "gz_reduce_step": (i32, [p, p, p, u64, dbl, i32, p, p, u64, p, p, p, u64, p, p]),
@@ -45,6 +46,7 @@ SIGNATURES = {
     "gz_stream_wait_u32_geq": (i32, [p, p, u32]),
     "gz_copy_blob": (i32, [p, p, p, u64, p]),
     "gz_copy_items": (i32, [p, u32, p]),
+    "gz_copy_items_sms": (i32, [p, u32, i32, p]),
     "gz_launch_count": (u64, []),
 }
 

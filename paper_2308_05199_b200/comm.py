@@ -40,6 +40,7 @@ from .collectives import _check_op, chunk_spans, scatter_counts
 from .schedule import Compress, Reduce, ring_allreduce_plan
 
 _ALIGN = 256
+AG_COPY_SMS = 24  # SMs left to the allgather's NVLink pulls while the previous owner's blob is decoded
 
 
 def _al(v: int) -> int:
@@ -102,6 +103,7 @@ class Communicator:
         self.launches_per_call = 0
         self.events = None  # list -> (label, cuda event) marks after every wait/launch (profiling)
         self.copy_stream = torch.cuda.Stream(self.device)  # allgather pulls
+        self.ag_mode = "copy"  # allgather: "multi" (one remote-read decode launch) or "copy" (pull, then local decode)
 
     # ------------------------------------------------------------------ setup
     def _setup(self, m_max: int):
@@ -356,6 +358,21 @@ class Communicator:
         s = self.stream.cuda_stream
         ws = self.ws
         launches = 0
+        if len(owners) > 1 and self.ag_mode == "multi":
+            # one launch decodes every owner's blob straight out of its memory
+            for j in owners:
+                self._wait(lay.ag_ready(j), e, s)
+            k = len(owners)
+            P = ctypes.c_void_p * k
+            blobs = P(*[self._addr(j, lay.own_off[0]) for j in owners])
+            scs = P(*[self._addr(j, lay.own_off[1]) for j in owners])
+            ns = (ctypes.c_uint64 * k)(*[msize(chunk_of(j)) for j in owners])
+            ys = P(*[chunk_ptr(out, chunk_of(j)) for j in owners])
+            L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s), "gz_decompress_multi")
+            self._mark("decode")
+            for j in owners:
+                self._signal(j, lay.ag_consumed(i), e, s)
+            return 1
         if len(owners) == 1:
             j = owners[0]
             c = chunk_of(j)
@@ -378,7 +395,8 @@ class Communicator:
                           lay.blob_cap),
                 _CopyItem(self._addr(j, lay.own_off[1]), self._addr(i, sc), None,
                           int(lib.gz_sidecar_bytes(msize(chunk_of(j))))))
-            L.check(lib.gz_copy_items(items, 2, cs), "gz_copy_items")
+            # the first pull has the GPU to itself; later ones run beside a decode
+            L.check(lib.gz_copy_items_sms(items, 2, AG_COPY_SMS if k else 0, cs), "gz_copy_items_sms")
             launches += 1
             self._signal(j, lay.ag_consumed(i), e, cs)
             ev = torch.cuda.Event()
@@ -388,8 +406,10 @@ class Communicator:
             c = chunk_of(j)
             self.stream.wait_event(landed[k])
             b, sc = lay.slot_off[k]
-            L.check(lib.gz_decompress_sidecar(self._addr(i, b), self._addr(i, sc), msize(c), ebf, chunk_ptr(out, c),
-                                              ws.status_ptr(), s), "gz_decompress_sidecar")
+            P = ctypes.c_void_p * 1
+            L.check(lib.gz_decompress_multi(P(self._addr(i, b)), P(self._addr(i, sc)), (ctypes.c_uint64 * 1)(msize(c)), 1,
+                                            ebf, P(chunk_ptr(out, c)), AG_COPY_SMS if k + 1 < len(owners) else 0,
+                                            ws.status_ptr(), s), "gz_decompress_multi")
             launches += 1
             self._mark("decode")
         return launches

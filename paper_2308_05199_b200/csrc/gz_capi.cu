@@ -15,7 +15,6 @@ using namespace gz;
 
 namespace {
 
-constexpr size_t DEC_SMEM_BYTES = (size_t)WARPS * DEC_WARP_SMEM;  // per warp: value tile + two stagings
 constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-parameter budget)
 
 // kernels launched by this library (all entry points, all streams): lets a
@@ -264,6 +263,44 @@ PFN_waitValue32 p_wait32() {
 
 // experiments only: per-warp timestamps of the next compress launch
 
+namespace {
+template <int NSEG>
+int launch_decode(DecodeMultiArgs<NSEG>& a, cudaStream_t s, int reserve_sms = 0) {
+  const size_t smem = (size_t)WARPS * dec_warp_smem(NSEG);  // per warp: value tile + stagings
+  static int cap = -1, per_sm = 1;
+  if (cap < 0) {
+    grid_cap(k_tile_decode<NSEG>, smem, cap);
+    int dev = 0, sms = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    per_sm = std::max(1, cap / std::max(1, sms));
+  }
+  // leave `reserve_sms` SMs free (a concurrent NVLink copy)
+  const int lim = std::max(per_sm, cap - reserve_sms * per_sm);
+  const uint64_t want = (a.total_tiles + WARPS - 1) / WARPS;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)lim));
+  count_launch();
+  k_tile_decode<NSEG><<<grid, CTA_THREADS, smem, s>>>(a);
+  return (int)cudaGetLastError();
+}
+
+int decode_one(const uint8_t* blob, const void* sidecar, const float* local, int op, uint64_t n, double eb, float* y,
+               gz_status* d_status, gz_stream_t stream) {
+  DecodeMultiArgs<1> a;
+  std::memset(&a, 0, sizeof(a));
+  SidecarView sv = sidecar_view(sidecar, n);
+  a.seg[0] = DecSeg{blob, sv.tile_off, sv.widths, n, y, 0};
+  a.nseg = 1;
+  a.total_tiles = ntiles_of(n);
+  a.tw = 2.0 * eb;
+  a.local = local;
+  a.op = op;
+  a.st = reinterpret_cast<Status*>(d_status);
+  return launch_decode<1>(a, (cudaStream_t)stream);
+}
+
+}  // namespace
+
 extern "C" {
 
 int gz_debug_set_timestamps(void* p) {
@@ -326,25 +363,7 @@ int gz_decompress_reduce(const uint8_t* blob, const void* sidecar, const float* 
   if (op != OP_SUM && op != OP_MAX) return GZ_EINVAL;
   if (!blob || !sidecar || (!y && n) || (!local && n) || !d_status) return GZ_EINVAL;
   if (n == 0) return 0;
-  DecodeArgs a;
-  std::memset(&a, 0, sizeof(a));
-  SidecarView sv = sidecar_view(sidecar, n);
-  a.local = local;
-  a.op = op;
-  a.blob = blob;
-  a.tile_off = sv.tile_off;
-  a.widths = sv.widths;
-  a.n = n;
-  a.tw = 2.0 * eb;
-  a.y = y;
-  a.st = reinterpret_cast<Status*>(d_status);
-  static int cap = -1;
-  grid_cap(k_tile_decode, DEC_SMEM_BYTES, cap);
-  const uint64_t want = (ntiles_of(n) + WARPS - 1) / WARPS;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
-  count_launch();
-  k_tile_decode<<<grid, CTA_THREADS, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(a);
-  return (int)cudaGetLastError();
+  return decode_one(blob, sidecar, local, op, n, eb, y, d_status, stream);
 }
 
 int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, double eb, float* y,
@@ -352,23 +371,40 @@ int gz_decompress_sidecar(const uint8_t* blob, const void* sidecar, uint64_t n, 
   if (!check_eb(eb)) return GZ_EBOUND;
   if (!blob || !sidecar || (!y && n) || !d_status) return GZ_EINVAL;
   if (n == 0) return 0;
-  DecodeArgs a;
+  return decode_one(blob, sidecar, nullptr, 0, n, eb, y, d_status, stream);
+}
+
+int gz_decompress_multi(const uint8_t* const* blobs, const void* const* sidecars, const uint64_t* ns, uint32_t count,
+                        double eb, float* const* ys, int reserve_sms, gz_status* d_status, gz_stream_t stream) {
+  if (!check_eb(eb)) return GZ_EBOUND;
+  if (!blobs || !sidecars || !ns || !ys || !d_status || count > GZ_MAX_DECODE_SEGMENTS) return GZ_EINVAL;
+  DecodeMultiArgs<GZ_MAX_DECODE_SEGMENTS> a;
   std::memset(&a, 0, sizeof(a));
-  SidecarView sv = sidecar_view(sidecar, n);
-  a.blob = blob;
-  a.tile_off = sv.tile_off;
-  a.widths = sv.widths;
-  a.n = n;
+  uint64_t tiles = 0;
+  int k = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    if (ns[i] == 0) continue;
+    if (!blobs[i] || !sidecars[i] || !ys[i]) return GZ_EINVAL;
+    SidecarView sv = sidecar_view(sidecars[i], ns[i]);
+    a.seg[k++] = DecSeg{blobs[i], sv.tile_off, sv.widths, ns[i], ys[i], tiles};
+    tiles += ntiles_of(ns[i]);
+  }
+  if (k == 0) return 0;
+  a.nseg = k;
+  a.total_tiles = tiles;
   a.tw = 2.0 * eb;
-  a.y = y;
   a.st = reinterpret_cast<Status*>(d_status);
-  static int cap = -1;
-  grid_cap(k_tile_decode, DEC_SMEM_BYTES, cap);
-  const uint64_t want = (ntiles_of(n) + WARPS - 1) / WARPS;
-  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, (uint64_t)cap));
-  count_launch();
-  k_tile_decode<<<grid, CTA_THREADS, DEC_SMEM_BYTES, (cudaStream_t)stream>>>(a);
-  return (int)cudaGetLastError();
+  if (k == 1) {  // a single blob: the local two-stage decoder
+    DecodeMultiArgs<1> b;
+    std::memset(&b, 0, sizeof(b));
+    b.seg[0] = a.seg[0];
+    b.nseg = 1;
+    b.total_tiles = tiles;
+    b.tw = a.tw;
+    b.st = a.st;
+    return launch_decode<1>(b, (cudaStream_t)stream, reserve_sms);
+  }
+  return launch_decode<GZ_MAX_DECODE_SEGMENTS>(a, (cudaStream_t)stream, reserve_sms);
 }
 
 uint64_t gz_index_workspace_bytes(uint64_t payload_len) {
@@ -582,6 +618,10 @@ int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64
 }
 
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream) {
+  return gz_copy_items_sms(items, count, 0, stream);
+}
+
+int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget, gz_stream_t stream) {
   if (count == 0) return 0;
   if (!items || count > GZ_MAX_COPY_ITEMS) return GZ_EINVAL;
   CopyItems ci;
@@ -593,7 +633,8 @@ int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream)
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const unsigned gx = (unsigned)std::max(1, 4 * sms / (int)count);
+  const int use = sms_budget > 0 ? std::min(sms_budget, sms) : sms;  // 4 CTAs per SM of the budget
+  const unsigned gx = (unsigned)std::max(1, 4 * use / (int)count);
   count_launch();
   k_copy_items<<<dim3(gx, count), 256, 0, (cudaStream_t)stream>>>(ci);
   return (int)cudaGetLastError();

@@ -55,17 +55,6 @@ struct EncodeArgs {
   float* acc_out;          // optional: reduced values (f32)
 };
 
-struct DecodeArgs {
-  const float* local;      // optional: y = op(local, decoded) (reduce-scatter's last step)
-  int op;
-  const uint8_t* blob;     // header + payload (may be a peer pointer)
-  const uint64_t* tile_off;
-  const uint8_t* widths;
-  uint64_t n;
-  double tw;
-  float* y;
-  Status* st;
-};
 
 // Fused step: the received tile's bytes are staged synchronously and the
 // local values are loaded for the current tile only (one value buffer, one
@@ -78,7 +67,6 @@ constexpr int ENC_WARP_SMEM = STEP_BUFS * TILE_VALUES * 4 + (STEP_ASYNC_STAGE ? 
 __host__ __device__ constexpr int enc_warps(int src) {
   return src == 1 ? (STEP_ASYNC_STAGE ? 13 : (STEP_BUFS == 2 ? 16 : 24)) : 24;
 }
-constexpr int DEC_WARP_SMEM = TILE_VALUES * 4 + 2 * STAGE_BYTES;  // value tile + two stagings
 
 // -------------------------------------------------------------------------
 // small helpers
@@ -1106,75 +1094,130 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
 }
 
 // -------------------------------------------------------------------------
-// Decompress with sidecar offsets: persistent warps stride over tiles, the
-// next tile's compressed bytes prefetched (cp.async) while decoding.
-__global__ void __launch_bounds__(CTA_THREADS, 4) k_tile_decode(const DecodeArgs a) {
+// Decompress with sidecar offsets: persistent warps stride over the tiles of
+// up to NSEG blobs (the allgather decodes every owner's blob, read straight
+// from the owners' memory, in one launch); software pipeline: a tile's bytes
+// and widths are staged one iteration ahead, its offsets two ahead.
+struct DecSeg {
+  const uint8_t* blob;       // header + payload (may be a peer pointer)
+  const uint64_t* tile_off;  // sidecar
+  const uint8_t* widths;
+  uint64_t n;
+  float* y;
+  uint64_t tile_base;        // first global tile of this blob
+};
+template <int NSEG>
+struct DecodeMultiArgs {
+  DecSeg seg[NSEG];
+  int nseg;
+  uint64_t total_tiles;
+  double tw;
+  const float* local;      // NSEG == 1 only: y = op(local, decoded)
+  int op;
+  Status* st;
+};
+
+// Stages per warp: 2 (one tile ahead) for local blobs; 3 (two tiles ahead)
+// when decoding several blobs out of peer GPUs' memory, where the NVLink
+// latency needs more bytes in flight.
+__host__ __device__ constexpr int dec_stages(int nseg) { return nseg > 1 ? 3 : 2; }
+__host__ __device__ constexpr int dec_warp_smem(int nseg) { return TILE_VALUES * 4 + dec_stages(nseg) * STAGE_BYTES; }
+
+template <int NSEG>
+__global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiArgs<NSEG> a) {
+  constexpr int ST = dec_stages(NSEG), D = ST - 1;  // D tiles staged ahead
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* my = smem + warp * DEC_WARP_SMEM;
+  unsigned char* my = smem + warp * dec_warp_smem(NSEG);
   float* xs = reinterpret_cast<float*>(my);
-  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4);
-  uint32_t* stg1 = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4 + STAGE_BYTES);
+  uint32_t* stg = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4);
   init_step_table(s_step, a.tw);
   __syncthreads();
-  const uint64_t n = a.n;
-  const uint64_t nb = (n + BLOCK - 1) / BLOCK;
-  const uint64_t ntiles = (nb + TB - 1) / TB;
-  const int last_cnt = (int)(n - (nb - 1) * BLOCK);
-  const uint8_t* payload = a.blob + HEADER_BYTES;
+  const uint64_t total = a.total_tiles;
+  auto seg_of = [&](uint64_t t) -> int {
+    int k = 0;
+    if (NSEG > 1) {
+#pragma unroll 1
+      for (int i = 1; i < a.nseg; ++i)
+        if (a.seg[i].tile_base <= t) k = i;
+    }
+    return k;
+  };
+  struct Meta {
+    uint64_t ts, te;
+  };
+  auto offsets = [&](uint64_t t) -> Meta {
+    Meta m{0, 0};
+    if (t < total) {
+      const DecSeg& S = a.seg[seg_of(t)];
+      const uint64_t lt = t - S.tile_base;
+      m.ts = S.tile_off[lt];
+      m.te = S.tile_off[lt + 1];
+    }
+    return m;
+  };
+  // stage tile t into buffer bi (cp.async, caller commits); returns base, width
+  auto stage = [&](uint64_t t, const Meta& m, int bi, int& base, int& w) {
+    base = 0;
+    w = 0;
+    if (t < total) {
+      const DecSeg& S = a.seg[seg_of(t)];
+      base = stage_bytes<true>(stg + bi * STAGE_WORDS, S.blob + HEADER_BYTES, m.ts, m.te, lane);
+      w = S.widths[(t - S.tile_base) * TB + lane];
+    }
+  };
   const uint64_t stride = (uint64_t)gridDim.x * WARPS;
   uint64_t t = (uint64_t)blockIdx.x * WARPS + warp;
-  // software pipeline: tile t's bytes and widths are staged one iteration
-  // ahead, tile offsets two iterations ahead (they address the staging)
-  int buf = 0;
-  uint64_t ts = 0, te = 0, tsn = 0, ten = 0;
-  int base = 0, w = 0;
-  if (t < ntiles) {
-    ts = a.tile_off[t];
-    te = a.tile_off[t + 1];
-    base = stage_bytes<true>(stg0, payload, ts, te, lane);
-    w = a.widths[t * TB + lane];
-  }
-  cp_async_commit();
-  if (t + stride < ntiles) {
-    tsn = a.tile_off[t + stride];
-    ten = a.tile_off[t + stride + 1];
-  }
-  for (; t < ntiles; t += stride) {
-    const uint64_t tn = t + stride, tnn = tn + stride;
-    int basen = 0, wn = 0;
-    if (tn < ntiles) {
-      basen = stage_bytes<true>(buf ? stg0 : stg1, payload, tsn, ten, lane);
-      wn = a.widths[tn * TB + lane];
-    }
+  // software pipeline: tiles t .. t+(D-1)*stride staged, offsets of t+D*stride loaded
+  Meta md[D];
+  int bq[D], wq[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    md[d] = offsets(t + d * stride);
+    stage(t + d * stride, md[d], d, bq[d], wq[d]);
     cp_async_commit();
-    uint64_t tsnn = 0, tenn = 0;
-    if (tnn < ntiles) {
-      tsnn = a.tile_off[tnn];
-      tenn = a.tile_off[tnn + 1];
-    }
-    cp_async_wait_1();
+  }
+  Meta mnext = offsets(t + D * stride);
+  int bi = 0;  // buffer of tile t
+  for (; t < total; t += stride) {
+    const uint64_t tn = t + D * stride;
+    int bn, wn;
+    stage(tn, mnext, (bi + D) % ST, bn, wn);
+    cp_async_commit();
+    const Meta mnn = offsets(tn + stride);
+    // wait until tile t's group is complete (D newer groups may stay pending)
+    if (D == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
+    else cp_async_wait_1();
     __syncwarp();
-    uint32_t* stage = buf ? stg1 : stg0;
-    const uint64_t b0 = t * TB;
+    const uint32_t* stage_t = stg + bi * STAGE_WORDS;
+    const DecSeg& S = a.seg[seg_of(t)];
+    const uint64_t lt = t - S.tile_base;
+    const uint64_t n = S.n;
+    const uint64_t nb = (n + BLOCK - 1) / BLOCK;
+    const int last_cnt = (int)(n - (nb - 1) * BLOCK);
+    const uint64_t b0 = lt * TB;
     const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
     const uint64_t v0 = b0 * BLOCK;
     const int nval = (int)(n - v0 < (uint64_t)TILE_VALUES ? n - v0 : (uint64_t)TILE_VALUES);
-    const int wl = lane < nblk ? w : 0;
-    const int start = block_start(stage, base, (int)(te - ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
-    decode_row<0>(stage, base, start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
+    const int wl = lane < nblk ? wq[0] : 0;
+    const int start = block_start(stage_t, bq[0], (int)(md[0].te - md[0].ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
+    decode_row<0>(stage_t, bq[0], start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
-    if (a.local) drain_values_op(xs, a.local, a.op, a.y, v0, nval, lane);
-    else drain_values(xs, a.y, v0, nval, lane);
+    if (NSEG == 1 && a.local) drain_values_op(xs, a.local, a.op, S.y, v0, nval, lane);
+    else drain_values(xs, S.y, v0, nval, lane);
     __syncwarp();
-    buf ^= 1;
-    ts = tsn;
-    te = ten;
-    base = basen;
-    w = wn;
-    tsn = tsnn;
-    ten = tenn;
+#pragma unroll
+    for (int d = 0; d + 1 < D; ++d) {
+      md[d] = md[d + 1];
+      bq[d] = bq[d + 1];
+      wq[d] = wq[d + 1];
+    }
+    md[D - 1] = mnext;
+    bq[D - 1] = bn;
+    wq[D - 1] = wn;
+    mnext = mnn;
+    bi = (bi + 1) % ST;
   }
 }
 

@@ -20,6 +20,8 @@ def main():
     n = mib * (1 << 18)
     x = torch.from_numpy(O.smooth_field(n, 0.37 * rank)).to(dev)
     c = comm.Communicator(dist.group.WORLD, dev)
+    if len(sys.argv) > 2:
+        c.ag_mode = sys.argv[2]
     out = torch.empty_like(x)
     for _ in range(3):
         c.ring_allreduce(x, 1e-4, "sum", out)
