@@ -51,6 +51,7 @@ class Counters:
     n_messages: int = 0
     bytes_sent: int = 0
     raw_bytes_in: int = 0
+    blob_bytes_out: int = 0
 
     def as_dict(self) -> dict:
         return dict(self.__dict__)
@@ -143,6 +144,7 @@ def ring_reduce_scatter_virtual(buffers, eb, op="sum", ws: Workspace | None = No
         blob = compress(chunk(i, i), ebf, ws)
         counters[i].n_compress += 1
         counters[i].raw_bytes_in += 4 * blob.n
+        counters[i].blob_bytes_out += len(blob)
         sending.append(blob)
     owned = [None] * N
     for s in range(N - 1):
@@ -163,6 +165,7 @@ def ring_reduce_scatter_virtual(buffers, eb, op="sum", ws: Workspace | None = No
             if not last or _keep_blobs:
                 counters[i].n_compress += 1
                 counters[i].raw_bytes_in += 4 * blob.n
+                counters[i].blob_bytes_out += len(blob)
             if last:
                 owned[i] = acc
             nxt.append(blob)
@@ -222,6 +225,7 @@ def ring_allgather_virtual(chunks, eb, ws: Workspace | None = None, trace: Trace
         blobs.append(compress(owned[i], ebf, ws))
         counters[i].n_compress += 1
         counters[i].raw_bytes_in += 4 * owned[i].numel()
+        counters[i].blob_bytes_out += len(blobs[-1])
     gathered = _allgather_blobs(blobs, owned, lambda i: i, ws, trace, counters)
     return [torch.cat([gathered[i][c] for c in range(N)]) for i in range(N)]
 
@@ -297,13 +301,17 @@ def rd_allreduce_virtual(buffers, eb, op="sum", ws: Workspace | None = None, tra
     def comp(i):
         counters[i].n_compress += 1
         counters[i].raw_bytes_in += 4 * data[i].numel()
-        return compress(data[i], ebf, ws)
+        b = compress(data[i], ebf, ws)
+        counters[i].blob_bytes_out += len(b)
+        return b
 
     def fused(i, recv):  # data[i] = op(data[i], dec(recv)); returns compress(data[i])
         counters[i].n_decompress += 1
         counters[i].n_compress += 1
         counters[i].raw_bytes_in += 4 * data[i].numel()
-        return reduce_step(recv, data[i], ebf, op, ws, acc_out=data[i])
+        b = reduce_step(recv, data[i], ebf, op, ws, acc_out=data[i])
+        counters[i].blob_bytes_out += len(b)
+        return b
 
     def last(i, recv):  # data[i] = op(data[i], dec(recv))
         counters[i].n_decompress += 1
@@ -422,6 +430,7 @@ def binomial_scatter_virtual(root_data, N: int, eb, counts=None, root: int = 0, 
     counters[root].n_compress += N
     counters[root].raw_bytes_in += 4 * x.numel()
     sizes = seg.sizes
+    counters[root].blob_bytes_out += int(sum(sizes))
     if trace is not None:
         packed = seg.packed_bytes()
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
@@ -501,5 +510,6 @@ def run_collective(algorithm: str, inputs, *, ranks: int | None = None, eb: floa
     else:
         out = binomial_scatter_virtual(inputs, N, eb, counts, root, ws, trace, counters)
     raw = sum(c.raw_bytes_in for c in counters)
-    cr = None
+    out_b = sum(c.blob_bytes_out for c in counters)
+    cr = raw / out_b if raw > 0 and out_b > 0 else None  # simnet.py:276-278
     return out, Report(algorithm, N, [c.as_dict() for c in counters], cr, trace)

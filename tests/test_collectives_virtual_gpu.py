@@ -98,3 +98,69 @@ def test_zero_preservation(ws):
         outs, _ = C.run_collective(algo, zeros, eb=1e-4, workspace=ws)
         for o in outs:
             assert torch.all(o == 0.0)
+
+
+@pytest.mark.parametrize("N", [2, 4, 8, 16])
+def test_rd_power_of_two_op_counts(N, ws):
+    # pkg/tests/test_collectives.py:78-84
+    k = N.bit_length() - 1
+    rng = np.random.default_rng(N)
+    inputs = [rng.uniform(0, 1, 64).astype(np.float32) for _ in range(N)]
+    _, rep = C.run_collective("rd-allreduce", inputs, eb=1e-4, workspace=ws)
+    for c in rep.counters_per_rank:
+        assert (c["n_compress"], c["n_decompress"]) == (k, k)
+
+
+@pytest.mark.parametrize("N", [3, 6, 12])
+def test_rd_remainder_roles(N, ws):
+    # pkg/tests/test_collectives.py:86-99
+    pof2, r, k, role, _, _ = C.rd_plan(N)
+    rng = np.random.default_rng(N)
+    inputs = [rng.uniform(0, 1, 64).astype(np.float32) for _ in range(N)]
+    _, rep = C.run_collective("rd-allreduce", inputs, eb=1e-4, workspace=ws)
+    for i, c in enumerate(rep.counters_per_rank):
+        got = (c["n_compress"], c["n_decompress"])
+        assert got == {"donor": (1, 1), "absorber": (k + 1, k + 1), "direct": (k, k)}[role(i)]
+
+
+@pytest.mark.parametrize("eb", [1e-2, 1e-3, 1e-4])
+@pytest.mark.parametrize("N", [3, 4, 6, 7, 8])
+def test_rd_error_budget(eb, N, oracle, ws):
+    # pkg/tests/test_collectives.py:140-154: (N-1) eb at powers of two, 2 N eb otherwise
+    bound = (N - 1) * eb if N & (N - 1) == 0 else 2 * N * eb
+    for seed in range(3):
+        rng = np.random.default_rng(50 * seed + N)
+        bufs = [rng.uniform(0, 1, 60).astype(np.float32) for _ in range(N)]
+        outs, _ = C.run_collective("rd-allreduce", bufs, eb=eb, workspace=ws)
+        lossless = oracle.rd_allreduce(bufs, eb, raw=True)
+        for o, e in zip(outs, lossless):
+            assert max_err(e, o.cpu().numpy()) <= bound
+
+
+def _synth_images(images, width, height, seed):
+    # gzccl cli.py:170-181 (cfg5 image stacking input)
+    yy, xx = np.mgrid[0:height, 0:width]
+    base = 0.5 + 0.25 * np.sin(2 * np.pi * 3 * xx / width) * np.cos(2 * np.pi * 2 * yy / height)
+    rng = np.random.default_rng(seed)
+    return [np.clip(base + rng.uniform(-0.2, 0.2, base.shape), 0.0, 1.0).astype(np.float32).ravel()
+            for _ in range(images)]
+
+
+@pytest.mark.parametrize("eb,cr,psnr_db,maxerr", [(2e-4, 2.39, 85.7, 1.34e-3), (1e-4, 2.22, 91.7, 6.48e-4)])
+def test_image_stacking_cfg5(eb, cr, psnr_db, maxerr, oracle, ws):
+    # BASELINE.md section 2 (reference measured here): 8 images 512x512, ring-allreduce sum;
+    # outputs bit-exact with the oracle, so CR / PSNR / max error reproduce the reference's
+    imgs = _synth_images(8, 512, 512, 0)
+    outs, rep = C.run_collective("ring-allreduce", imgs, eb=eb, workspace=ws)
+    expect = oracle.ring_allreduce(imgs, eb)
+    for o, e in zip(outs, expect):
+        assert o.cpu().numpy().tobytes() == e.tobytes()
+    ref = np.concatenate(oracle.ring_allreduce(imgs, eb, raw=True)).astype(np.float64)
+    got = np.concatenate([o.cpu().numpy() for o in outs]).astype(np.float64)
+    err = np.abs(ref - got)
+    mse = float(np.mean((ref - got) ** 2))
+    rng_ = float(ref.max() - ref.min())
+    assert rep.compression_ratio == pytest.approx(cr, abs=0.01)
+    assert 10 * np.log10(rng_ ** 2 / mse) == pytest.approx(psnr_db, abs=0.05)
+    assert float(err.max()) == pytest.approx(maxerr, rel=0.01)
+    assert float(err.max()) <= 8 * eb
