@@ -330,7 +330,7 @@ def bench_allreduce(args):
     torch.cuda.synchronize()
     dist.barrier()
     times, step_t = [], []
-    launches0 = int(lib.gz_launch_count())
+    launches0 = int(lib.gz_launch_count()) + c.graph_launches
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             dist.barrier()
@@ -341,7 +341,7 @@ def bench_allreduce(args):
             e1.record(stream)
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1) * 1e-3)
-    launches = int(lib.gz_launch_count()) - launches0
+    launches = int(lib.gz_launch_count()) + c.graph_launches - launches0  # eager launches + graph replays
     # fused-step kernel durations: CUDA-event marks after every wait/launch of
     # the same call, on extra calls after the timed loop (marks perturb timing)
     for _ in range(3):

@@ -103,6 +103,11 @@ class Communicator:
         self.launches_per_call = 0
         self.events = None  # list -> (label, cuda event) marks after every wait/launch (profiling)
         self.copy_stream = torch.cuda.Stream(self.device)  # allgather pulls
+        self.use_graphs = True  # replay repeated ring calls from a captured CUDA graph
+        self.graph_launches = 0  # kernels executed by graph replays (not seen by gz_launch_count)
+        self.capture_stream = torch.cuda.Stream(self.device)
+        self._graph_cache = {}
+        self._last_key = None
         self.ag_mode = "copy"  # allgather: "multi" (one remote-read decode launch) or "copy" (pull, then local decode)
 
     # ------------------------------------------------------------------ setup
@@ -129,8 +134,16 @@ class Communicator:
                 L.check(lib.gz_ipc_open_handle(ctypes.create_string_buffer(hb, hsz), ctypes.byref(ptr)),
                         "gz_ipc_open_handle")
                 self._peer.append(ptr.value)
+        # consumed flags start "free" (1): the first call needs no special case
+        flags = self._buf[: 4 * self.layout.flag_words].view(torch.int32)
+        flags[self.layout.rs_consumed() // 4] = 1
+        for j in range(self.world):
+            flags[self.layout.ag_consumed(j) // 4] = 1
+        torch.cuda.synchronize(self.device)
         self._n = m_max
         self.epoch = 0
+        self._graph_cache = {}
+        self._last_key = None
         dist.barrier(group=self.group)
 
     def _close(self):
@@ -143,6 +156,8 @@ class Communicator:
         self._peer = None
         self._buf = None
         self._n = None
+        self._graph_cache = {}
+        self._last_key = None
         _scatter_close(self)
         _rd_close(self)
 
@@ -170,10 +185,20 @@ class Communicator:
         L.check(L.lib().gz_stream_wait_u32_geq(s, self._addr(self.rank, off), value), "gz_stream_wait_u32_geq")
         self._mark("wait")
 
+    # ring flags are binary semaphores (constant values, so a call can be
+    # captured in a CUDA graph and replayed): post = write 1 into the peer's
+    # flag; take = wait for 1 on our own flag, then reset it to 0
+    def _post(self, r: int, off: int, s: int):
+        self._signal(r, off, 1, s)
+
+    def _take(self, off: int, s: int):
+        self._wait(off, 1, s)
+        self._signal(self.rank, off, 0, s)
+
     def _mark(self, label: str):
         if self.events is not None:
             ev = torch.cuda.Event(enable_timing=True)
-            ev.record(self.stream)
+            ev.record(torch.cuda.current_stream(self.device))
             self.events.append((label, ev))
 
     # ------------------------------------------------------------ collectives
@@ -190,8 +215,34 @@ class Communicator:
             out.copy_(x)
             return out
         spans = chunk_spans(x.numel(), self.world)
-        self._ring("allreduce", x, spans, _check_eb(eb), _check_op(op), out)
+        self._run_graphed("allreduce", x, spans, _check_eb(eb), _check_op(op), out)
         return out
+
+    def _run_graphed(self, mode, x, spans, ebf, opc, out):
+        """Run one ring collective; a call repeated on the same tensors and
+        parameters is captured once into a CUDA graph and then replayed (one
+        launch of the whole schedule: kernels, peer flags, the allgather's
+        side-stream pulls), which removes the per-call host cost."""
+        key = (mode, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), ebf, opc)
+        if self.use_graphs and self.events is None and not torch.cuda.is_current_stream_capturing():
+            g = self._graph_cache.get(key) if self._n is not None else None
+            if g is not None:
+                g[0].replay()
+                self.graph_launches += g[1]
+                self.launches_per_call = g[1]
+                return
+            if self._n is not None and self._last_key == key and len(self._graph_cache) < 16:
+                g = torch.cuda.CUDAGraph()
+                s0 = torch.cuda.current_stream(self.device)
+                with torch.cuda.graph(g, stream=self.capture_stream):
+                    self._ring(mode, x, spans, ebf, opc, out)
+                s0.wait_stream(self.capture_stream)
+                self._graph_cache[key] = (g, self.launches_per_call)
+                g.replay()
+                self.graph_launches += self.launches_per_call
+                return
+        self._last_key = key
+        self._ring(mode, x, spans, ebf, opc, out)
 
     def ring_reduce_scatter(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
         """Per-rank ring_reduce_scatter_c (collectives.py:258-291): returns the
@@ -206,7 +257,7 @@ class Communicator:
         if N == 1:
             out.copy_(x)
             return out
-        self._ring("reduce_scatter", x, spans, _check_eb(eb), _check_op(op), out)
+        self._run_graphed("reduce_scatter", x, spans, _check_eb(eb), _check_op(op), out)
         return out
 
     def ring_allgather(self, chunk: torch.Tensor, eb: float, out: torch.Tensor | None = None):
@@ -246,7 +297,8 @@ class Communicator:
         self._setup(m_max)
         lib = L.lib()
         lay = self.layout
-        s = self.stream.cuda_stream
+        cur = torch.cuda.current_stream(self.device)  # (a capture stream while recording a graph)
+        s = cur.cuda_stream
         ws = self.ws
         tws = ws.tile_ws(int(lib.gz_workspace_bytes(m_max)))
         e = self.epoch + 1
@@ -265,22 +317,20 @@ class Communicator:
 
         def wait_own_blob_free():
             # peers must have consumed our previous own blob
-            if self.epoch:
-                for j in range(N):
-                    if j != i:
-                        self._wait(lay.ag_consumed(j), self.epoch, s)
+            for j in range(N):
+                if j != i:
+                    self._take(lay.ag_consumed(j), s)
 
         def own_ready():
             for j in range(N):
                 if j != i:
-                    self._signal(j, lay.ag_ready(i), e, s)
+                    self._post(j, lay.ag_ready(i), s)
 
         launches = 0
         self._mark("start")
         if mode in ("allreduce", "reduce_scatter"):
             # the right neighbour must have consumed our previous writes
-            if self.epoch:
-                self._wait(lay.rs_consumed(), self.epoch, s)
+            self._take(lay.rs_consumed(), s)
             for p in ring_allreduce_plan(N, i):
                 if isinstance(p, Compress):
                     # step 0: compress the local chunk straight into right's slot 0
@@ -290,9 +340,9 @@ class Communicator:
                                             tws.numel(), ws.status_ptr(), s), "gz_compress")
                     launches += 2
                     self._mark("compress")
-                    self._signal(p.dst, lay.rs_full(p.slot), e, s)
+                    self._post(p.dst, lay.rs_full(p.slot), s)
                 elif isinstance(p, Reduce):
-                    self._wait(lay.rs_full(p.slot), e, s)
+                    self._take(lay.rs_full(p.slot), s)
                     inb, insc = slot(i, p.slot)
                     if p.last and mode == "reduce_scatter":
                         # decode + reduce into the owned chunk; nothing to re-compress
@@ -317,7 +367,7 @@ class Communicator:
                     launches += 2
                     self._mark("reduce_last" if p.last else "reduce")
                     if not p.last:
-                        self._signal(p.dst, lay.rs_full(p.slot + 1), e, s)
+                        self._post(p.dst, lay.rs_full(p.slot + 1), s)
                     else:
                         own_ready()
         if mode == "allgather":
@@ -335,18 +385,13 @@ class Communicator:
             # compress-once allgather; owner j's chunk is chunk_of(j)
             owners = [(i - 1 - k) % N for k in range(N - 1)]  # the order the ring delivers them
             chunk_of = (lambda j: (j + 1) % N) if mode == "allreduce" else (lambda j: j)
-            launches += self._allgather_pull(owners, chunk_of, chunk_ptr, msize, out, ebf, e)
-        else:
-            # nobody pulled our (absent) own blob this epoch
-            for j in range(N):
-                if j != i:
-                    self._signal(j, lay.ag_consumed(i), e, s)
+            launches += self._allgather_pull(owners, chunk_of, chunk_ptr, msize, out, ebf, cur)
         # our slots are free again: the left neighbour may write the next call's steps
-        self._signal(left, lay.rs_consumed(), e, s)
+        self._post(left, lay.rs_consumed(), s)
         self.epoch = e
         self.launches_per_call = launches
 
-    def _allgather_pull(self, owners, chunk_of, chunk_ptr, msize, out, ebf, e) -> int:
+    def _allgather_pull(self, owners, chunk_of, chunk_ptr, msize, out, ebf, cur) -> int:
         """A side stream pulls each owner's blob + sidecar over NVLink into our
         (free) reduce-scatter slots with one bulk copy and releases the owner;
         the main stream decodes it from local HBM as soon as it has landed,
@@ -355,13 +400,13 @@ class Communicator:
         lib = L.lib()
         lay = self.layout
         N, i = self.world, self.rank
-        s = self.stream.cuda_stream
+        s = cur.cuda_stream
         ws = self.ws
         launches = 0
         if len(owners) > 1 and self.ag_mode == "multi":
             # one launch decodes every owner's blob straight out of its memory
             for j in owners:
-                self._wait(lay.ag_ready(j), e, s)
+                self._take(lay.ag_ready(j), s)
             k = len(owners)
             P = ctypes.c_void_p * k
             blobs = P(*[self._addr(j, lay.own_off[0]) for j in owners])
@@ -371,24 +416,25 @@ class Communicator:
             L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s), "gz_decompress_multi")
             self._mark("decode")
             for j in owners:
-                self._signal(j, lay.ag_consumed(i), e, s)
+                self._post(j, lay.ag_consumed(i), s)
             return 1
         if len(owners) == 1:
             j = owners[0]
             c = chunk_of(j)
-            self._wait(lay.ag_ready(j), e, s)
+            self._take(lay.ag_ready(j), s)
             L.check(lib.gz_decompress_sidecar(self._addr(j, lay.own_off[0]), self._addr(j, lay.own_off[1]), msize(c),
                                               ebf, chunk_ptr(out, c), ws.status_ptr(), s), "gz_decompress_sidecar")
             self._mark("decode")
-            self._signal(j, lay.ag_consumed(i), e, s)
+            self._post(j, lay.ag_consumed(i), s)
             return 1
         cs = self.copy_stream.cuda_stream
         rs_done = torch.cuda.Event()
-        rs_done.record(self.stream)
+        rs_done.record(cur)
         self.copy_stream.wait_event(rs_done)
         landed = []
         for k, j in enumerate(owners):
-            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(j)), e), "gz_stream_wait_u32_geq")
+            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(j)), 1), "gz_stream_wait_u32_geq")
+            L.check(lib.gz_stream_write_u32(cs, self._addr(i, lay.ag_ready(j)), 0), "gz_stream_write_u32")
             b, sc = lay.slot_off[k]
             items = (_CopyItem * 2)(
                 _CopyItem(self._addr(j, lay.own_off[0]), self._addr(i, b), self._addr(j, lay.len_off + 8 * N),
@@ -398,13 +444,13 @@ class Communicator:
             # the first pull has the GPU to itself; later ones run beside a decode
             L.check(lib.gz_copy_items_sms(items, 2, AG_COPY_SMS if k else 0, cs), "gz_copy_items_sms")
             launches += 1
-            self._signal(j, lay.ag_consumed(i), e, cs)
+            self._post(j, lay.ag_consumed(i), cs)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)
             landed.append(ev)
         for k, j in enumerate(owners):
             c = chunk_of(j)
-            self.stream.wait_event(landed[k])
+            cur.wait_event(landed[k])
             b, sc = lay.slot_off[k]
             P = ctypes.c_void_p * 1
             L.check(lib.gz_decompress_multi(P(self._addr(i, b)), P(self._addr(i, sc)), (ctypes.c_uint64 * 1)(msize(c)), 1,
