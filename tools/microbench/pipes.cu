@@ -21,6 +21,13 @@ __global__ void k(double* out, float* outf, double a, float af) {
       if (OP == 5) { f[c] = __fadd_rn(f[c], af); }                 // FADD
       if (OP == 6) { li[c] = __double_as_longlong(d[c] = __dadd_rn((double)(li[c] & 1023), a)); } // I2F.F64 + DADD
       if (OP == 7) { f[c] = floorf(f[c]) + af; }                    // FRND f32
+      if (OP == 8 && (c & 1) == 0) {                                // FADD2 (two lanes of f32x2)
+        unsigned long long v = ((unsigned long long)__float_as_uint(f[c + 1]) << 32) | __float_as_uint(f[c]);
+        const unsigned long long w = ((unsigned long long)__float_as_uint(af) << 32) | __float_as_uint(af);
+        asm("add.rn.f32x2 %0, %0, %1;" : "+l"(v) : "l"(w));
+        f[c] = __uint_as_float((unsigned)v); f[c + 1] = __uint_as_float((unsigned)(v >> 32));
+      }
+      if (OP == 9) { li[c] = (li[c] << 1) ^ (li[c] >> 31); }        // int shift/xor (ALU)
     }
   }
   double s = 0; float sf = 0;
@@ -45,6 +52,7 @@ int main() {
   run<0>("DADD", o, of); run<1>("DFMA", o, of); run<2>("F2F.f32->f64, DMUL, F2F.f64->f32", o, of);
   run<3>("F2F f64->f32->f64 + DADD", o, of); run<4>("floor f64 + DADD", o, of); run<5>("FADD", o, of);
   run<6>("I2F.F64 + DADD", o, of); run<7>("floorf + FADD", o, of);
+  run<8>("FADD2 (per f32 lane)", o, of); run<9>("SHF/LOP int", o, of);
   cudaError_t e = cudaDeviceSynchronize(); printf("status %s\n", cudaGetErrorString(e));
   return 0;
 }
