@@ -1,30 +1,31 @@
 """Compressed collectives across GPUs: one process per GPU over NVLink peer memory.
 
 The per-rank schedules are the reference's (collectives.py:215-308,
-467-532); the simulated network (simnet.py) is replaced by CUDA-IPC mapped
-buffers:
+349-424, 467-532); the simulated network (simnet.py) is replaced by CUDA-IPC
+mapped buffers:
 
 ring reduce-scatter (collectives.py:258-291)
-    step 0   gz_compress(local chunk i)                 -> right's slot[0]
-    step s   wait slot[s]; gz_reduce_step(slot[s], local chunk (i-s-1) mod N)
-             -> right's slot[s+1]   (s < N-2)
+    step 0   gz_compress(local chunk i)                  -> own out slot[0]
+    step s   wait "left's slot[s] ready"; gz_reduce_step(left's slot[s] read
+             over NVLink, local chunk (i-s-1) mod N)
+             -> own out slot[s+1]   (s < N-2)
              -> own blob + owned f32 chunk (i+1) mod N (s = N-2)
-    The fused kernel's output stores ARE the send: they land in the peer's
-    HBM over NVLink while the kernel runs.  Block offsets travel in the
-    sidecar, so no size message is needed (the size exchange is overlapped
-    with compression, north_star).
+    The fused kernel reads the left neighbour's blob straight out of its
+    HBM (the loads overlap the decode/encode of other tiles).  Block offsets
+    and widths travel in the sidecar, so no size message is needed (the size
+    exchange is overlapped with compression, north_star).
 compress-once allgather (collectives.py:215-244)
-    the owner's blob is compressed once (the last RS step) and every other
-    rank decodes it straight out of the owner's memory (peer loads); the
-    bytes are never recompressed, so the allreduce error stays <= N * eb.
-binomial scatter (collectives.py:467-532)
-    the root compresses all N segments in one launch; each rank pulls its own
-    blob from the root (or from its tree parent) and decodes it.
+    the owner's blob is compressed once (the last RS step); every other rank
+    pulls those bytes into a local landing slot on a side stream and decodes
+    them while the next pull is in flight; the bytes are never recompressed,
+    so the allreduce error stays <= N * eb.
+recursive doubling (collectives.py:349-424) and binomial scatter (467-532)
+    see Communicator.rd_allreduce / Communicator.binomial_scatter.
 
 Synchronisation is stream-ordered (cuStreamWriteValue32 / WaitValue32 on
-peer-mapped flag words): no host round trips, no spinning kernels.  An epoch
-counter per call makes the flags reusable; "consumed" flags stop a rank from
-overwriting a peer's slot or its own blob before the previous call has read it.
+peer-mapped flag words): no host round trips, no spinning kernels.  The ring
+flags are binary semaphores ("consumed" flags start free), so a repeated
+call is captured once into a CUDA graph and replayed.
 """
 
 from __future__ import annotations
@@ -48,7 +49,8 @@ def _al(v: int) -> int:
 
 
 class _Layout:
-    """Carve one device buffer into flags, RS slots and the owned blob."""
+    """Carve one device buffer into flags, RS output slots, allgather landing
+    slots and the owned blob."""
 
     def __init__(self, world: int, m_max: int):
         lib = L.lib()
@@ -60,9 +62,13 @@ class _Layout:
         off = _al(4 * self.flag_words)
         self.len_off = off  # u64 lengths: slots[world] + own[1]
         off += _al(8 * (world + 1))
-        self.slot_off = []
+        self.slot_off = []  # reduce-scatter outputs of this rank, pulled by the right neighbour
         for _ in range(max(world - 1, 0)):
             self.slot_off.append((off, off + self.blob_cap))
+            off += self.blob_cap + self.sc_bytes
+        self.land_off = []  # allgather landing slots (owners' blobs pulled here)
+        for _ in range(max(world - 1, 0)):
+            self.land_off.append((off, off + self.blob_cap))
             off += self.blob_cap + self.sc_bytes
         self.own_off = (off, off + self.blob_cap)
         off += self.blob_cap + self.sc_bytes
@@ -333,17 +339,18 @@ class Communicator:
             self._take(lay.rs_consumed(), s)
             for p in ring_allreduce_plan(N, i):
                 if isinstance(p, Compress):
-                    # step 0: compress the local chunk straight into right's slot 0
-                    b, sc = slot(p.dst, p.slot)
+                    # step 0: compress the local chunk into our output slot 0; the right
+                    # neighbour's fused step reads it straight out of our memory
+                    b, sc = slot(i, p.slot)
                     L.check(lib.gz_compress(chunk_ptr(x, p.chunk), msize(p.chunk), ebf, 32, b, lay.blob_cap,
-                                            self._addr(p.dst, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
+                                            self._addr(i, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
                                             tws.numel(), ws.status_ptr(), s), "gz_compress")
                     launches += 2
                     self._mark("compress")
                     self._post(p.dst, lay.rs_full(p.slot), s)
                 elif isinstance(p, Reduce):
                     self._take(lay.rs_full(p.slot), s)
-                    inb, insc = slot(i, p.slot)
+                    inb, insc = slot(left, p.slot)  # the left neighbour's output, over NVLink
                     if p.last and mode == "reduce_scatter":
                         # decode + reduce into the owned chunk; nothing to re-compress
                         L.check(lib.gz_decompress_reduce(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc,
@@ -353,8 +360,8 @@ class Communicator:
                         continue
                     # fused decompress(recv) + op + compress; the output stores are the send
                     if not p.last:
-                        ob, osc = slot(p.dst, p.slot + 1)
-                        olen = self._addr(p.dst, lay.len_off + 8 * (p.slot + 1))
+                        ob, osc = slot(i, p.slot + 1)
+                        olen = self._addr(i, lay.len_off + 8 * (p.slot + 1))
                         acc = None
                     else:
                         wait_own_blob_free()  # our own blob is read by every peer in the allgather
@@ -435,7 +442,7 @@ class Communicator:
         for k, j in enumerate(owners):
             L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(j)), 1), "gz_stream_wait_u32_geq")
             L.check(lib.gz_stream_write_u32(cs, self._addr(i, lay.ag_ready(j)), 0), "gz_stream_write_u32")
-            b, sc = lay.slot_off[k]
+            b, sc = lay.land_off[k]
             items = (_CopyItem * 2)(
                 _CopyItem(self._addr(j, lay.own_off[0]), self._addr(i, b), self._addr(j, lay.len_off + 8 * N),
                           lay.blob_cap),
@@ -451,7 +458,7 @@ class Communicator:
         for k, j in enumerate(owners):
             c = chunk_of(j)
             cur.wait_event(landed[k])
-            b, sc = lay.slot_off[k]
+            b, sc = lay.land_off[k]
             P = ctypes.c_void_p * 1
             L.check(lib.gz_decompress_multi(P(self._addr(i, b)), P(self._addr(i, sc)), (ctypes.c_uint64 * 1)(msize(c)), 1,
                                             ebf, P(chunk_ptr(out, c)), AG_COPY_SMS if k + 1 < len(owners) else 0,
