@@ -196,6 +196,27 @@ def ring_allgather(chunks, eb, trace=None, raw=False):
     return [np.concatenate([g[i][c] for c in range(N)]) if N > 1 else owned[i].copy() for i in range(N)]
 
 
+def cprp2p_allgather(chunks, eb, trace=None):
+    """cprp2p_allgather, collectives.py:311-341: every hop decompresses and
+    re-compresses what it forwards."""
+    owned = [np.ascontiguousarray(c, "<f4") for c in chunks]
+    N = len(owned)
+    if N == 1:
+        return [owned[0].copy()]
+    gathered = [{i: owned[i]} for i in range(N)]
+    current = list(owned)
+    for s in range(N - 1):
+        sent = [compress(current[i], eb) for i in range(N)]
+        if trace is not None:
+            for i in range(N):
+                trace.append(("cp", s, i, (i + 1) % N, sent[i]))
+        for i in range(N):
+            vals = decompress(sent[(i - 1) % N])
+            gathered[i][(i - 1 - s) % N] = vals
+            current[i] = vals
+    return [np.concatenate([gathered[i][c] for c in range(N)]) for i in range(N)]
+
+
 def rd_plan(N: int):
     """RecursiveDoublingPlan, collectives.py:48-86: (pof2, r, steps, role, remapped, actual)."""
     pof2 = 1 << (N.bit_length() - 1)

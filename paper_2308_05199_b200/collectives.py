@@ -350,6 +350,138 @@ def rd_allreduce_virtual(buffers, eb, op="sum", ws: Workspace | None = None, tra
 
 
 # ---------------------------------------------------------------------------
+# comparators (collectives.py:311-341, 545-566)
+# ---------------------------------------------------------------------------
+
+
+def cprp2p_allgather_virtual(chunks, eb, ws: Workspace | None = None, trace: Trace | None = None,
+                             counters: list | None = None) -> list[torch.Tensor]:
+    """cprp2p_allgather (collectives.py:311-341): the compress-per-hop baseline;
+    every hop decompresses and re-compresses, so a chunk that travelled h hops
+    carries up to h * eb of error (N-1 compressions and decompressions per rank)."""
+    ebf = _check_eb(eb)
+    ws = ws or Workspace()
+    N = len(chunks)
+    owned = _dev_inputs(chunks, N, ws.device)
+    _check_finite(owned)
+    if counters is None:
+        counters = [Counters() for _ in range(N)]
+    if N == 1:
+        return [owned[0].clone()]
+    gathered = [{i: owned[i]} for i in range(N)]
+    current = list(owned)
+    for s in range(N - 1):
+        sent = []
+        for i in range(N):
+            b = compress(current[i], ebf, ws)
+            counters[i].n_compress += 1
+            counters[i].raw_bytes_in += 4 * current[i].numel()
+            counters[i].blob_bytes_out += len(b)
+            sent.append(b)
+            if trace is not None:
+                trace.add(i, (i + 1) % N, b)
+            counters[i].n_messages += 1
+            counters[i].bytes_sent += len(b)
+        for i in range(N):
+            vals = decompress(sent[(i - 1) % N], ws)
+            counters[i].n_decompress += 1
+            gathered[i][(i - 1 - s) % N] = vals
+            current[i] = vals
+    return [torch.cat([gathered[i][c] for c in range(N)]) for i in range(N)]
+
+
+def _raw_op(op: str, local: torch.Tensor, received: torch.Tensor) -> torch.Tensor:
+    # _apply_op (collectives.py:32-39) on verbatim f32 payloads
+    if op == "sum":
+        return local + received
+    return torch.where(torch.isnan(local) | (local > received), local, received)  # np.maximum(local, received)
+
+
+def _raw_send(trace, counters, i, dst, t: torch.Tensor):
+    if trace is not None:
+        trace.add(i, dst, t.detach().cpu().numpy().astype("<f4").tobytes())
+    counters[i].n_messages += 1
+    counters[i].bytes_sent += 4 * t.numel()
+
+
+def lossless_ring_reduce_scatter(buffers, op="sum", ws: Workspace | None = None, trace: Trace | None = None,
+                                 counters: list | None = None):
+    """ring_reduce_scatter_c with the RawTransport (the "lossless-*" twins,
+    collectives.py:94-111, 560-566): verbatim f32 messages, no codec."""
+    _check_op(op)
+    ws = ws or Workspace()
+    N = len(buffers)
+    bufs = _dev_inputs(buffers, N, ws.device)
+    n = _require_equal(bufs)
+    _check_finite(bufs)
+    if counters is None:
+        counters = [Counters() for _ in range(N)]
+    if N == 1:
+        return [bufs[0].clone()]
+    spans = chunk_spans(n, N)
+    acc = [[b[lo:hi].clone() for lo, hi in spans] for b in bufs]
+    for s in range(N - 1):
+        sent = [acc[i][(i - s) % N] for i in range(N)]
+        for i in range(N):
+            _raw_send(trace, counters, i, (i + 1) % N, sent[i])
+        sent = [t.clone() for t in sent]
+        for i in range(N):
+            c_in = (i - s - 1) % N
+            acc[i][c_in] = _raw_op(op, acc[i][c_in], sent[(i - 1) % N])
+    return [acc[i][(i + 1) % N] for i in range(N)]
+
+
+def _lossless_allgather_owned(owned, chunk_of, trace, counters):
+    N = len(owned)
+    gathered = [{chunk_of(i): owned[i]} for i in range(N)]
+    carry = list(owned)
+    for s in range(N - 1):
+        for i in range(N):
+            _raw_send(trace, counters, i, (i + 1) % N, carry[i])
+        carry = [carry[(i - 1) % N] for i in range(N)]
+        for i in range(N):
+            gathered[i][chunk_of((i - 1 - s) % N)] = carry[i].clone()
+    return gathered
+
+
+def lossless_ring_allgather(chunks, ws: Workspace | None = None, trace: Trace | None = None,
+                            counters: list | None = None):
+    ws = ws or Workspace()
+    N = len(chunks)
+    owned = _dev_inputs(chunks, N, ws.device)
+    _check_finite(owned)
+    if counters is None:
+        counters = [Counters() for _ in range(N)]
+    if N == 1:
+        return [owned[0].clone()]
+    g = _lossless_allgather_owned(owned, lambda i: i, trace, counters)
+    return [torch.cat([g[i][c] for c in range(N)]) for i in range(N)]
+
+
+def lossless_ring_allreduce(buffers, op="sum", ws: Workspace | None = None, trace: Trace | None = None,
+                            counters: list | None = None):
+    ws = ws or Workspace()
+    N = len(buffers)
+    if counters is None:
+        counters = [Counters() for _ in range(N)]
+    owned = lossless_ring_reduce_scatter(buffers, op, ws, trace, counters)
+    if N == 1:
+        return owned
+    g = _lossless_allgather_owned(owned, lambda i: (i + 1) % N, trace, counters)
+    return [torch.cat([g[i][c] for c in range(N)]) for i in range(N)]
+
+
+def lossless_binomial_scatter(root_data, N: int, counts=None, root: int = 0, ws: Workspace | None = None):
+    """binomial_scatter_c with the RawTransport: every rank gets its slice verbatim."""
+    ws = ws or Workspace()
+    x = _dev_inputs([root_data], 1, ws.device)[0]
+    _check_finite([x])
+    counts = scatter_counts(x.numel(), N, counts)
+    lo = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return [x[lo[r]:lo[r + 1]].clone() for r in range(N)]
+
+
+# ---------------------------------------------------------------------------
 # binomial-tree scatter (collectives.py:432-532)
 # ---------------------------------------------------------------------------
 
@@ -463,6 +595,11 @@ ALGORITHMS = {
     "ring-allreduce": "allreduce",
     "rd-allreduce": "allreduce",
     "binomial-scatter": "scatter",
+    "cprp2p-allgather": "allgather",
+    "lossless-allgather": "allgather",
+    "lossless-reduce-scatter": "reduce_scatter",
+    "lossless-allreduce": "allreduce",
+    "lossless-scatter": "scatter",
 }
 
 
@@ -491,7 +628,7 @@ def run_collective(algorithm: str, inputs, *, ranks: int | None = None, eb: floa
     the root's buffer and ``ranks`` gives the communicator size.
     """
     family = get_algorithm(algorithm)
-    if eb is None:
+    if eb is None and not algorithm.startswith("lossless-"):
         raise ValueError("the error-bounded codec needs an error bound (eb)")
     ws = workspace or Workspace()
     trace = Trace() if record_payloads else None
@@ -501,6 +638,16 @@ def run_collective(algorithm: str, inputs, *, ranks: int | None = None, eb: floa
     counters = [Counters() for _ in range(N)]
     if algorithm == "rd-allreduce":
         out = rd_allreduce_virtual(inputs, eb, reduce_op, ws, trace, counters)
+    elif algorithm == "cprp2p-allgather":
+        out = cprp2p_allgather_virtual(inputs, eb, ws, trace, counters)
+    elif algorithm == "lossless-allreduce":
+        out = lossless_ring_allreduce(inputs, reduce_op, ws, trace, counters)
+    elif algorithm == "lossless-reduce-scatter":
+        out = lossless_ring_reduce_scatter(inputs, reduce_op, ws, trace, counters)
+    elif algorithm == "lossless-allgather":
+        out = lossless_ring_allgather(inputs, ws, trace, counters)
+    elif algorithm == "lossless-scatter":
+        out = lossless_binomial_scatter(inputs, N, counts, root, ws)
     elif family == "allreduce":
         out = ring_allreduce_virtual(inputs, eb, reduce_op, ws, trace, counters)
     elif family == "reduce_scatter":

@@ -204,6 +204,31 @@ def ring_cases(codec, collectives, simnet):
         out[pre + "msg_dst"] = np.array([t[1] for t in net.trace], np.int64)
         rows.append(("rd-allreduce", N, n, op, eb))
         k += 1
+    # comparators (collectives.py:311-341, 545-566): the compress-per-hop allgather and the lossless twins
+    cmp_cfgs = [("cprp2p-allgather", 2, 300, "sum", 1e-4), ("cprp2p-allgather", 4, 1000, "sum", 1e-3),
+                ("cprp2p-allgather", 7, 64, "sum", 1e-4), ("lossless-allreduce", 4, 1000, "sum", 1e-4),
+                ("lossless-allreduce", 3, 77, "max", 1e-4), ("lossless-reduce-scatter", 5, 999, "sum", 1e-4),
+                ("lossless-allgather", 4, 500, "sum", 1e-4)]
+    for algo, N, n, op, eb in cmp_cfgs:
+        rng = np.random.default_rng(1000 + k)
+        if algo.endswith("allgather"):
+            lens = [int(rng.integers(0, n + 1)) for _ in range(N)]
+            inputs = [smooth(m, 0.37 * r) for r, m in enumerate(lens)]
+        else:
+            inputs = [smooth(n, 0.37 * r) + rng.normal(0, 1e-3, n).astype(np.float32) for r in range(N)]
+        net = simnet.Network(simnet.CommunicatorSpec(N), record_payloads=True)
+        outputs, rep = simnet.run_collective(net, algo, inputs, eb=eb, reduce_op=op, compute_accuracy=False)
+        pre = f"c{k}_"
+        out[pre + "meta"] = np.array([N, n, 1 if op == "max" else 0], np.int64)
+        out[pre + "algo"] = np.array(algo)
+        out[pre + "eb"] = np.array(eb)
+        pack_list(pre + "in", [np.asarray(a, np.float32) for a in inputs], out)
+        pack_list(pre + "out", [np.asarray(o, np.float32) for o in outputs], out)
+        pack_list(pre + "msg", [np.frombuffer(t[3], np.uint8).copy() for t in net.trace], out)
+        out[pre + "msg_src"] = np.array([t[0] for t in net.trace], np.int64)
+        out[pre + "msg_dst"] = np.array([t[1] for t in net.trace], np.int64)
+        rows.append((algo, N, n, op, eb))
+        k += 1
     out["count"] = np.array(k)
     np.savez_compressed(os.path.join(HERE, "ring_cases.npz"), **out)
     return rows

@@ -164,3 +164,29 @@ def test_image_stacking_cfg5(eb, cr, psnr_db, maxerr, oracle, ws):
     assert 10 * np.log10(rng_ ** 2 / mse) == pytest.approx(psnr_db, abs=0.05)
     assert float(err.max()) == pytest.approx(maxerr, rel=0.01)
     assert float(err.max()) <= 8 * eb
+
+
+def test_lossless_scatter_exact(ws):
+    rng = np.random.default_rng(5)
+    data = rng.normal(0, 1, 1000).astype(np.float32)
+    outs, _ = C.run_collective("lossless-scatter", data, ranks=4, counts=[100, 200, 300, 400], workspace=ws)
+    lo = 0
+    for o, c in zip(outs, [100, 200, 300, 400]):
+        assert o.cpu().numpy().tobytes() == data[lo:lo + c].tobytes()
+        lo += c
+
+
+@pytest.mark.parametrize("N", [2, 4, 7])
+def test_cprp2p_hop_error(N, oracle, ws):
+    # collectives.py:311-316: a chunk that travelled h hops carries up to h * eb
+    eb = 1e-3
+    rng = np.random.default_rng(N)
+    chunks = [rng.uniform(0, 1, 100).astype(np.float32) for _ in range(N)]
+    outs, rep = C.run_collective("cprp2p-allgather", chunks, eb=eb, workspace=ws)
+    for i, o in enumerate(outs):
+        o = o.cpu().numpy()
+        for c in range(N):
+            h = (i - c) % N
+            assert np.max(np.abs(o[100 * c:100 * (c + 1)] - chunks[c])) <= max(h, 0) * eb + 1e-7
+    for cnt in rep.counters_per_rank:
+        assert (cnt["n_compress"], cnt["n_decompress"]) == (N - 1, N - 1)

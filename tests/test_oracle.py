@@ -98,6 +98,14 @@ def test_oracle_ring_matches_reference(case, oracle):
         outs = oracle.ring_reduce_scatter(case.inputs, case.eb, case.op, trace)
     elif case.algo == "rd-allreduce":
         outs = oracle.rd_allreduce(case.inputs, case.eb, case.op, trace)
+    elif case.algo == "cprp2p-allgather":
+        outs = oracle.cprp2p_allgather(case.inputs, case.eb, trace)
+    elif case.algo == "lossless-allreduce":
+        outs = oracle.ring_allreduce(case.inputs, case.eb, case.op, trace, raw=True)
+    elif case.algo == "lossless-reduce-scatter":
+        outs = oracle.ring_reduce_scatter(case.inputs, case.eb, case.op, trace, raw=True)
+    elif case.algo == "lossless-allgather":
+        outs = oracle.ring_allgather(case.inputs, case.eb, trace, raw=True)
     else:
         outs = oracle.ring_allgather(case.inputs, case.eb, trace)
     assert len(outs) == case.N
