@@ -147,6 +147,15 @@ int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream)
  * decoder launched with reserve_sms = sms_budget (allgather pipeline) */
 int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget, gz_stream_t stream);
 
+/* ---- fixed-rate baseline codec (codec.py:442-489, a comparator) --------------
+ * Uniform quantisation of the whole buffer over [min, max] to `bits` (1..16)
+ * per value, "<QBff" header (n, bits, lo, hi) + codes LSB-first.  ws8: 8 bytes
+ * of device scratch.  The host validates a blob's header before decoding. */
+uint64_t gz_fr_bound(uint64_t n, uint32_t bits);
+int gz_fr_compress(const float* x, uint64_t n, uint32_t bits, uint8_t* out, uint64_t out_cap, uint64_t* d_len,
+                   void* ws8, gz_status* d_status, gz_stream_t stream);
+int gz_fr_decompress(const uint8_t* blob, uint64_t n, uint32_t bits, float* y, gz_stream_t stream);
+
 /* number of kernels this library has launched so far (all entry points) */
 uint64_t gz_launch_count(void);
 

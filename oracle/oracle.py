@@ -349,3 +349,58 @@ def smooth_field(n: int, phase: float = 0.0) -> np.ndarray:
     """SURVEY §8(d) cfg1/cfg2 field: f32(0.5 sin(2πi/65536 + φ) + 0.25 sin(2πi/4099 + φ))."""
     i = np.arange(n, dtype=np.float64)
     return (0.5 * np.sin(2 * np.pi * i / 65536 + phase) + 0.25 * np.sin(2 * np.pi * i / 4099 + phase)).astype(np.float32)
+
+
+# ---------------------------------------------------------------------------
+# fixed-rate baseline codec (codec.py:442-489), numpy restatement
+# ---------------------------------------------------------------------------
+FR_HEADER_BYTES = 17  # struct "<QBff": n, bits, lo, hi
+
+
+def fixed_rate_compress(data, bits_per_value: int) -> bytes:
+    import struct
+
+    x = np.ascontiguousarray(data, "<f4").reshape(-1)
+    b = int(bits_per_value)
+    if not 1 <= b <= 16:
+        raise ValueError(f"bits_per_value must be in [1, 16], got {b}")
+    n = x.size
+    lo = float(x.min()) if n else 0.0
+    hi = float(x.max()) if n else 0.0
+    head = struct.pack("<QBff", n, b, lo, hi)
+    if n == 0:
+        return head
+    levels = (1 << b) - 1
+    if hi > lo:
+        v = (x.astype(np.float64) - lo) / (hi - lo) * levels
+        q = np.floor(np.abs(v) + 0.5) * np.sign(v)
+        q = np.clip(q, 0, levels).astype(np.uint32)
+    else:
+        q = np.zeros(n, dtype=np.uint32)
+    bitsarr = ((q[:, None] >> np.arange(b, dtype=np.uint32)[None, :]) & 1).astype(np.uint8).reshape(-1)
+    return head + np.packbits(bitsarr, bitorder="little").tobytes()
+
+
+def fixed_rate_decompress(blob) -> np.ndarray:
+    import struct
+
+    blob = bytes(blob)
+    if len(blob) < FR_HEADER_BYTES:
+        raise ValueError(f"blob too short for fixed-rate header ({len(blob)} bytes)")
+    n, b, lo, hi = struct.unpack_from("<QBff", blob)
+    if not 1 <= b <= 16:
+        raise ValueError(f"invalid bits_per_value {b} in header")
+    expect = (n * b + 7) // 8
+    payload = np.frombuffer(blob, dtype=np.uint8, offset=FR_HEADER_BYTES)
+    if payload.size != expect:
+        raise ValueError(f"payload is {payload.size} bytes, expected {expect}")
+    if n == 0:
+        return np.empty(0, dtype=np.float32)
+    bitsarr = np.unpackbits(payload, bitorder="little")[: n * b].reshape(n, b).astype(np.uint32)
+    q = (bitsarr << np.arange(b, dtype=np.uint32)[None, :]).sum(axis=1)
+    levels = (1 << b) - 1
+    if hi > lo:
+        vals = lo + q.astype(np.float64) * ((hi - lo) / levels)
+    else:
+        vals = np.full(n, lo, dtype=np.float64)
+    return vals.astype(np.float32)

@@ -21,6 +21,8 @@ from .codec import (
     compress_blocks,
     decompress,
     decompress_block,
+    fixed_rate_compress,
+    fixed_rate_decompress,
     worst_case_blob_bytes,
 )
 
@@ -38,6 +40,8 @@ __all__ = [
     "Workspace",
     "compress",
     "compress_blocks",
+    "fixed_rate_compress",
+    "fixed_rate_decompress",
     "decompress",
     "decompress_block",
     "worst_case_blob_bytes",

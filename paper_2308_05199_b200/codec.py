@@ -401,6 +401,61 @@ def decompress_block(payload, table: BlockTable, index_: int, workspace: Workspa
     return decompress(payload[off:end], workspace)
 
 
+FR_HEADER = struct.Struct("<QBff")  # codec.py:48
+FR_HEADER_BYTES = FR_HEADER.size  # 17
+
+
+def fixed_rate_compress(data, bits_per_value: int, workspace: Workspace | None = None, stream=None):
+    """Fixed-rate baseline (codec.py:442-468): uniform quantisation over
+    [min, max] to ``bits_per_value`` bits, ``17 + ceil(n*b/8)`` bytes.  Host
+    input -> ``bytes`` (byte-identical to the reference); CUDA tensor -> a
+    CUDA uint8 tensor holding the same bytes."""
+    b = int(bits_per_value)
+    if not 1 <= b <= 16:
+        raise ValueError(f"bits_per_value must be in [1, 16], got {b}")
+    x, on_dev = _as_device_f32(data, workspace.device if workspace is not None else None)
+    ws = _ws_for(workspace, x.device)
+    n = x.numel()
+    lib = L.lib()
+    cap = int(lib.gz_fr_bound(n, b))
+    out = torch.empty(cap, dtype=torch.uint8, device=x.device)
+    scratch = ws.tile_ws(16)
+    ws.reset_status(stream)
+    L.check(lib.gz_fr_compress(x.data_ptr(), n, b, out.data_ptr(), cap, ws.len_ptr(), scratch.data_ptr(),
+                               ws.status_ptr(), _stream(stream)), "gz_fr_compress")
+    st = ws.read_status(stream)
+    if st[0] != _NONE:
+        raise ValueError(f"non-finite value at offset {int(st[0])}")  # codec.py:83-85
+    blob = out[: int(st[4])]
+    return blob if on_dev else blob.cpu().numpy().tobytes()
+
+
+def fixed_rate_decompress(blob, workspace: Workspace | None = None, stream=None):
+    """Inverse of :func:`fixed_rate_compress` (codec.py:471-489), same errors."""
+    if isinstance(blob, torch.Tensor) and blob.is_cuda:
+        dev_blob, host_head = blob, blob[:FR_HEADER_BYTES].cpu().numpy().tobytes()
+        total = blob.numel()
+    else:
+        raw = bytes(blob)
+        dev_blob, host_head, total = None, raw[:FR_HEADER_BYTES], len(raw)
+    if len(host_head) < FR_HEADER_BYTES:
+        raise DecodeError(f"blob too short for fixed-rate header ({len(host_head)} bytes)")
+    n, b, lo, hi = FR_HEADER.unpack_from(host_head)
+    if not 1 <= b <= 16:
+        raise DecodeError(f"invalid bits_per_value {b} in header")
+    expect = (n * b + 7) // 8
+    if total - FR_HEADER_BYTES != expect:
+        raise DecodeError(f"payload is {total - FR_HEADER_BYTES} bytes, expected {expect}")
+    dev = _device_of(workspace.device if workspace is not None else (dev_blob.device if dev_blob is not None else None))
+    if dev_blob is None:
+        dev_blob = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(dev)
+    y = torch.empty(n, dtype=torch.float32, device=dev)
+    L.check(L.lib().gz_fr_decompress(dev_blob.data_ptr(), n, b, y.data_ptr(), _stream(stream)), "gz_fr_decompress")
+    if isinstance(blob, torch.Tensor) and blob.is_cuda:
+        return y
+    return y.cpu().numpy()
+
+
 def worst_case_blob_bytes(n: int) -> int:
     """Upper bound on compressed size: header plus all-raw blocks (codec.py:492-494)."""
     return HEADER_BYTES + -(-n // BLOCK) * (1 + 4 + 4 * BLOCK)

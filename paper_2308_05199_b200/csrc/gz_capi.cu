@@ -10,6 +10,7 @@
 #include "../../include/gzccl.h"
 #include "gz_codec.cu"
 #include "gz_index.cu"
+#include "gz_fixed.cu"
 
 using namespace gz;
 
@@ -637,6 +638,38 @@ int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget,
   const unsigned gx = (unsigned)std::max(1, 4 * use / (int)count);
   count_launch();
   k_copy_items<<<dim3(gx, count), 256, 0, (cudaStream_t)stream>>>(ci);
+  return (int)cudaGetLastError();
+}
+
+// ---- fixed-rate baseline codec (codec.py:442-489) -------------------------
+uint64_t gz_fr_bound(uint64_t n, uint32_t bits) { return FR_HEADER_BYTES + (n * (uint64_t)bits + 7) / 8 + 16; }
+
+int gz_fr_compress(const float* x, uint64_t n, uint32_t bits, uint8_t* out, uint64_t out_cap, uint64_t* d_len,
+                   void* ws8, gz_status* d_status, gz_stream_t stream) {
+  if (bits < 1 || bits > 16) return GZ_EINVAL;
+  if ((!x && n) || !out || !d_len || !ws8 || !d_status) return GZ_EINVAL;
+  if (out_cap < FR_HEADER_BYTES + (n * (uint64_t)bits + 7) / 8) return GZ_ECAPACITY;
+  cudaStream_t s = (cudaStream_t)stream;
+  int* mm = reinterpret_cast<int*>(ws8);
+  const int init[2] = {0x7FFFFFFF, (int)0x80000000};
+  cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  const uint64_t groups = (n + 31) / 32;
+  if (n) {
+    count_launch();
+    k_fr_minmax<<<592, 256, 0, s>>>(x, n, mm, reinterpret_cast<Status*>(d_status));
+  }
+  count_launch();
+  k_fr_encode<<<(unsigned)std::max<uint64_t>(1, (groups + 255) / 256), 256, 0, s>>>(x, n, (int)bits, mm, out, d_len);
+  return (int)cudaGetLastError();
+}
+
+int gz_fr_decompress(const uint8_t* blob, uint64_t n, uint32_t bits, float* y, gz_stream_t stream) {
+  if (bits < 1 || bits > 16) return GZ_EINVAL;
+  if (!blob || (!y && n)) return GZ_EINVAL;
+  if (n == 0) return 0;
+  const uint64_t groups = (n + 31) / 32;
+  count_launch();
+  k_fr_decode<<<(unsigned)((groups + 255) / 256), 256, 0, (cudaStream_t)stream>>>(blob, n, (int)bits, y);
   return (int)cudaGetLastError();
 }
 

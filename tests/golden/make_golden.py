@@ -257,6 +257,29 @@ def scatter_cases(codec, collectives, simnet):
     return len(cfgs)
 
 
+def fixed_rate_cases(codec):
+    """Fixed-rate baseline codec (codec.py:442-489): inputs, bits, blobs, decoded values."""
+    cfgs = [(0, 8), (1, 4), (31, 1), (32, 3), (1000, 8), (4099, 16), (777, 5), (20000, 12), (64, 7), (100, 2)]
+    out = {}
+    datas, blobs, ys = [], [], []
+    for k, (n, b) in enumerate(cfgs):
+        rng = np.random.default_rng(2000 + k)
+        x = smooth(n, 0.2 * k) + rng.normal(0, 0.01, n).astype(np.float32) if k % 3 else rng.uniform(-5, 5, n).astype(np.float32)
+        if k == 9:
+            x = np.full(n, 3.25, np.float32)  # hi == lo
+        blob = codec.fixed_rate_compress(x, b)
+        datas.append(np.asarray(x, np.float32))
+        blobs.append(np.frombuffer(blob, np.uint8).copy())
+        ys.append(codec.fixed_rate_decompress(blob))
+    out["bits"] = np.array([b for _, b in cfgs], np.int64)
+    pack_list("x", datas, out)
+    pack_list("blob", blobs, out)
+    pack_list("y", ys, out)
+    out["count"] = np.array(len(cfgs))
+    np.savez_compressed(os.path.join(HERE, "fixed_rate_cases.npz"), **out)
+    return len(cfgs)
+
+
 def digests(codec):
     x = smooth(1 << 24)
     d = {"cfg1_input_sha256": hashlib.sha256(x.tobytes()).hexdigest()}
@@ -277,5 +300,6 @@ if __name__ == "__main__":
             f.write(codec.compress(data, eb))
     print("codec cases:", codec_cases(codec))
     print("ring cases:", len(ring_cases(codec, collectives, simnet)))
+    print("fixed-rate cases:", fixed_rate_cases(codec))
     print("scatter cases:", scatter_cases(codec, collectives, simnet))
     print("digests:", digests(codec))

@@ -104,3 +104,10 @@ def golden_data(seed):
     n, eb = GOLDEN_CASES[seed]
     rng = np.random.default_rng(seed)
     return rng.uniform(-1.0, 1.0, n).astype(np.float32), eb
+
+
+def fixed_rate_cases():
+    """(x, bits, blob bytes, decoded y) from the reference's fixed_rate_compress."""
+    z = np.load(os.path.join(GOLDEN_DIR, "fixed_rate_cases.npz"))
+    xs, blobs, ys = _unpack(z, "x"), _unpack(z, "blob"), _unpack(z, "y")
+    return [(xs[k], int(z["bits"][k]), blobs[k].tobytes(), ys[k]) for k in range(int(z["count"]))]

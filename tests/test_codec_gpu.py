@@ -173,3 +173,29 @@ def test_workspace_reuse_and_determinism(ws, oracle):
     for _ in range(5):
         assert bytes(gz.compress(x, 1e-4, ws)) == a
     assert bytes(gz.compress(x, 1e-4, gz.Workspace())) == a
+
+
+FR = G.fixed_rate_cases()
+
+
+@pytest.mark.parametrize("k", range(len(FR)))
+def test_fixed_rate_matches_reference(k, ws):
+    # codec.py:442-489 (the comparator), byte-identical blobs and values
+    x, b, blob, y = FR[k]
+    assert gz.fixed_rate_compress(x, b, ws) == blob
+    assert gz.fixed_rate_decompress(blob, ws).tobytes() == y.tobytes()
+    dev = gz.fixed_rate_compress(torch.from_numpy(x).cuda(), b, ws)
+    assert dev.cpu().numpy().tobytes() == blob
+    assert gz.fixed_rate_decompress(dev, ws).cpu().numpy().tobytes() == y.tobytes()
+
+
+def test_fixed_rate_errors(ws):
+    with pytest.raises(ValueError, match="bits_per_value"):
+        gz.fixed_rate_compress(np.zeros(4, np.float32), 17)
+    blob = gz.fixed_rate_compress(np.arange(10, dtype=np.float32), 4, ws)
+    with pytest.raises(gz.DecodeError, match="expected"):
+        gz.fixed_rate_decompress(blob[:-1])
+    with pytest.raises(gz.DecodeError, match="too short"):
+        gz.fixed_rate_decompress(blob[:5])
+    with pytest.raises(ValueError, match="offset 3"):
+        gz.fixed_rate_compress(np.array([0, 1, 2, np.inf], np.float32), 4, ws)

@@ -126,3 +126,13 @@ def test_oracle_scatter_matches_reference(case, oracle):
         assert o.tobytes() == e.tobytes()
     assert [t[2] for t in trace] == case.msgs
     assert [t[0] for t in trace] == list(case.src) and [t[1] for t in trace] == list(case.dst)
+
+
+FR = G.fixed_rate_cases()
+
+
+@pytest.mark.parametrize("k", range(len(FR)))
+def test_oracle_fixed_rate_matches_reference(k, oracle):
+    x, b, blob, y = FR[k]
+    assert oracle.fixed_rate_compress(x, b) == blob
+    assert oracle.fixed_rate_decompress(blob).tobytes() == y.tobytes()
