@@ -108,6 +108,35 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
                    int op, float* acc_out, uint8_t* blob_out, uint64_t blob_out_cap, uint64_t* d_len_out,
                    void* sidecar_out, void* ws, uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream);
 
+/* ---- generalized step: plain compress or fused step, blob or slotted I/O ----
+ * Slotted form (the reduce-scatter's intermediate messages, never seen by a
+ * user): tile t's bytes at out_slots + t * 4224 (128-aligned, gz_slots_bytes),
+ * its byte count in out_sizes[t], the block widths in out_widths[t*32 ..] --
+ * the same bytes as the blob's tile t, without the gather that makes them
+ * contiguous; the consumer's fused step reads them in place (in_slots).
+ * in_blob == in_slots == NULL: plain compression of `local`. */
+typedef struct {
+  const uint8_t* in_blob;
+  const void* in_sidecar;
+  const uint8_t* in_slots;
+  const uint32_t* in_sizes;
+  const uint8_t* in_widths;
+  uint8_t* blob_out;
+  uint64_t blob_out_cap;
+  uint64_t* d_len_out;
+  void* sidecar_out;
+  uint8_t* out_slots;
+  uint32_t* out_sizes;
+  uint8_t* out_widths;
+} gz_step_io;
+uint64_t gz_slots_bytes(uint64_t m);
+int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,
+            uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream);
+/* y = op(local, decode(slotted input io->in_*)): a reduce-scatter's last step
+ * without re-compression (collectives.py:285-290) */
+int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* y,
+                   gz_status* d_status, gz_stream_t stream);
+
 /* ---- multi-segment compression (binomial scatter root) ----------------------
  * compress_blocks (codec.py:408-427): nseg independent blobs, blob i written
  * at payload + seg_blob_off[i] (host-planned worst-case slots). */

@@ -48,6 +48,9 @@ SIGNATURES = {
     "gz_copy_items": (i32, [p, u32, p]),
     "gz_copy_items_sms": (i32, [p, u32, i32, p]),
     "gz_launch_count": (u64, []),
+    "gz_slots_bytes": (u64, [u64]),
+    "gz_step": (i32, [p, p, u64, dbl, i32, p, p, u64, p, p]),
+    "gz_step_reduce": (i32, [p, p, u64, dbl, i32, p, p, p]),
     "gz_fr_bound": (u64, [u64, u32]),
     "gz_fr_compress": (i32, [p, u64, u32, p, u64, p, p, p, p]),
     "gz_fr_decompress": (i32, [p, u64, u32, p, p]),

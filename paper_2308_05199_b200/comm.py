@@ -62,10 +62,19 @@ class _Layout:
         off = _al(4 * self.flag_words)
         self.len_off = off  # u64 lengths: slots[world] + own[1]
         off += _al(8 * (world + 1))
-        self.slot_off = []  # reduce-scatter outputs of this rank, pulled by the right neighbour
+        # reduce-scatter outputs of this rank in slotted form (tile t at t * 4224,
+        # sizes, widths), read in place by the right neighbour's fused step
+        nt = int(lib.gz_num_tiles(m_max))
+        self.slots_bytes = _al(int(lib.gz_slots_bytes(m_max)))
+        self.slot_off = []
         for _ in range(max(world - 1, 0)):
-            self.slot_off.append((off, off + self.blob_cap))
-            off += self.blob_cap + self.sc_bytes
+            sl = off
+            off += self.slots_bytes
+            sz = off
+            off += _al(4 * nt)
+            wd = off
+            off += _al(32 * nt)
+            self.slot_off.append((sl, sz, wd))
         self.land_off = []  # allgather landing slots (owners' blobs pulled here)
         for _ in range(max(world - 1, 0)):
             self.land_off.append((off, off + self.blob_cap))
@@ -317,9 +326,20 @@ class Communicator:
         def msize(c):
             return spans[c][1] - spans[c][0]
 
-        def slot(r, k):
-            b, sc = lay.slot_off[k]
-            return self._addr(r, b), self._addr(r, sc)
+        def slot(r, k):  # (slots, sizes, widths) of rank r's reduce-scatter output k
+            sl, sz, wd = lay.slot_off[k]
+            return self._addr(r, sl), self._addr(r, sz), self._addr(r, wd)
+
+        def step(inp, local, n_, acc, out_slot=None, out_blob=None):
+            io = _StepIO()
+            if inp is not None:
+                io.in_slots, io.in_sizes, io.in_widths = inp
+            if out_slot is not None:
+                io.out_slots, io.out_sizes, io.out_widths = out_slot
+            else:
+                io.blob_out, io.blob_out_cap, io.d_len_out, io.sidecar_out = out_blob
+            L.check(lib.gz_step(ctypes.byref(io), local, n_, ebf, opc, acc, tws.data_ptr(), tws.numel(),
+                                ws.status_ptr(), s), "gz_step")
 
         def wait_own_blob_free():
             # peers must have consumed our previous own blob
@@ -339,39 +359,34 @@ class Communicator:
             self._take(lay.rs_consumed(), s)
             for p in ring_allreduce_plan(N, i):
                 if isinstance(p, Compress):
-                    # step 0: compress the local chunk into our output slot 0; the right
-                    # neighbour's fused step reads it straight out of our memory
-                    b, sc = slot(i, p.slot)
-                    L.check(lib.gz_compress(chunk_ptr(x, p.chunk), msize(p.chunk), ebf, 32, b, lay.blob_cap,
-                                            self._addr(i, lay.len_off + 8 * p.slot), sc, None, tws.data_ptr(),
-                                            tws.numel(), ws.status_ptr(), s), "gz_compress")
-                    launches += 2
+                    # step 0: compress the local chunk into our output slot 0 (slotted: no
+                    # gather); the right neighbour's fused step reads it in place
+                    step(None, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot))
+                    launches += 1
                     self._mark("compress")
                     self._post(p.dst, lay.rs_full(p.slot), s)
                 elif isinstance(p, Reduce):
                     self._take(lay.rs_full(p.slot), s)
-                    inb, insc = slot(left, p.slot)  # the left neighbour's output, over NVLink
+                    inp = slot(left, p.slot)  # the left neighbour's output, read over NVLink
                     if p.last and mode == "reduce_scatter":
                         # decode + reduce into the owned chunk; nothing to re-compress
-                        L.check(lib.gz_decompress_reduce(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc,
-                                                         out.data_ptr(), ws.status_ptr(), s), "gz_decompress_reduce")
+                        io = _StepIO()
+                        io.in_slots, io.in_sizes, io.in_widths = inp
+                        L.check(lib.gz_step_reduce(ctypes.byref(io), chunk_ptr(x, p.chunk), msize(p.chunk), ebf,
+                                                   opc, out.data_ptr(), ws.status_ptr(), s), "gz_step_reduce")
                         launches += 1
                         self._mark("reduce_last")
                         continue
-                    # fused decompress(recv) + op + compress; the output stores are the send
+                    # fused decompress(recv) + op + compress
                     if not p.last:
-                        ob, osc = slot(i, p.slot + 1)
-                        olen = self._addr(i, lay.len_off + 8 * (p.slot + 1))
-                        acc = None
+                        step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot + 1))
+                        launches += 1
                     else:
                         wait_own_blob_free()  # our own blob is read by every peer in the allgather
-                        ob, osc = self._addr(i, lay.own_off[0]), self._addr(i, lay.own_off[1])
-                        olen = self._addr(i, lay.len_off + 8 * N)
-                        acc = chunk_ptr(out, p.chunk)
-                    L.check(lib.gz_reduce_step(inb, insc, chunk_ptr(x, p.chunk), msize(p.chunk), ebf, opc, acc, ob,
-                                               lay.blob_cap, olen, osc, tws.data_ptr(), tws.numel(), ws.status_ptr(),
-                                               s), "gz_reduce_step")
-                    launches += 2
+                        step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), chunk_ptr(out, p.chunk),
+                             out_blob=(self._addr(i, lay.own_off[0]), lay.blob_cap,
+                                       self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1])))
+                        launches += 2
                     self._mark("reduce_last" if p.last else "reduce")
                     if not p.last:
                         self._post(p.dst, lay.rs_full(p.slot + 1), s)
@@ -478,6 +493,13 @@ class Communicator:
         self.last_compression_ratio = round(4 * m / ln, 4) if ln else None
         return self.last_compression_ratio
 
+
+
+class _StepIO(ctypes.Structure):  # gz_step_io (include/gzccl.h)
+    _fields_ = [("in_blob", ctypes.c_void_p), ("in_sidecar", ctypes.c_void_p), ("in_slots", ctypes.c_void_p),
+                ("in_sizes", ctypes.c_void_p), ("in_widths", ctypes.c_void_p), ("blob_out", ctypes.c_void_p),
+                ("blob_out_cap", ctypes.c_uint64), ("d_len_out", ctypes.c_void_p), ("sidecar_out", ctypes.c_void_p),
+                ("out_slots", ctypes.c_void_p), ("out_sizes", ctypes.c_void_p), ("out_widths", ctypes.c_void_p)]
 
 
 class _CopyItem(ctypes.Structure):

@@ -157,6 +157,7 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   int rc = (int)cudaGetLastError();
   if (rc) return rc;
   if (g_dbg_flags & 1) return 0;
+  if (a.slotted_out) return 0;  // slotted output: the consumer reads the slots
   // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
   static int gcap = -1;
   if (gcap < 0) {
@@ -290,7 +291,7 @@ int decode_one(const uint8_t* blob, const void* sidecar, const float* local, int
   DecodeMultiArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = DecSeg{blob, sv.tile_off, sv.widths, n, y, 0};
+  a.seg[0] = DecSeg{blob, sv.tile_off, sv.widths, n, y, 0, nullptr};
   a.nseg = 1;
   a.total_tiles = ntiles_of(n);
   a.tw = 2.0 * eb;
@@ -387,7 +388,7 @@ int gz_decompress_multi(const uint8_t* const* blobs, const void* const* sidecars
     if (ns[i] == 0) continue;
     if (!blobs[i] || !sidecars[i] || !ys[i]) return GZ_EINVAL;
     SidecarView sv = sidecar_view(sidecars[i], ns[i]);
-    a.seg[k++] = DecSeg{blobs[i], sv.tile_off, sv.widths, ns[i], ys[i], tiles};
+    a.seg[k++] = DecSeg{blobs[i], sv.tile_off, sv.widths, ns[i], ys[i], tiles, nullptr};
     tiles += ntiles_of(ns[i]);
   }
   if (k == 0) return 0;
@@ -503,6 +504,81 @@ uint64_t gz_segments_workspace_bytes(const uint64_t* h_counts, uint32_t nseg) {
   uint64_t tiles = 0;
   for (uint32_t i = 0; i < nseg; ++i) tiles += ntiles_of(h_counts[i]);
   return ws_bytes_for_tiles(tiles);
+}
+
+int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,
+            uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream) {
+  if (!check_eb(eb)) return GZ_EBOUND;
+  if (op != OP_SUM && op != OP_MAX) return GZ_EINVAL;
+  if (!io || (!local && m) || !ws || !d_status) return GZ_EINVAL;
+  const bool fused = io->in_blob || io->in_slots;
+  const bool slotted = io->out_slots != nullptr;
+  if (fused && !io->in_slots && !io->in_sidecar) return GZ_EINVAL;
+  if (io->in_slots && (!io->in_sizes || !io->in_widths)) return GZ_EINVAL;
+  if (slotted && (!io->out_sizes || !io->out_widths || (reinterpret_cast<uintptr_t>(io->out_slots) & 127))) return GZ_EINVAL;
+  if (!slotted && (!io->blob_out || !io->d_len_out || !aligned16(io->blob_out))) return GZ_EINVAL;
+  if (!slotted && io->blob_out_cap < gz_compress_bound(m)) return GZ_ECAPACITY;
+  if (ws_bytes < gz_workspace_bytes(m)) return GZ_EINVAL;
+  EncodeArgs<1> a;
+  std::memset(&a, 0, sizeof(a));
+  const WsView wv = carve(ws, ntiles_of(m));
+  a.ws = wv.hdr;
+  a.tile_rel = wv.tile_rel;
+  a.scratch = wv.scratch;
+  if (slotted) {
+    a.seg[0] = Seg{local, m, nullptr, nullptr, nullptr, io->out_widths, 0, 0, 0, 0};
+    a.tile_rel = io->out_sizes;
+    a.scratch = io->out_slots;
+    a.slotted_out = 1;
+    // the gather that would reset the tile-claim counter is skipped
+    cudaMemsetAsync(&wv.hdr->claim, 0, sizeof(unsigned int), (cudaStream_t)stream);
+  } else {
+    SidecarView so = sidecar_view(io->sidecar_out, m);
+    a.seg[0] = Seg{local, m, io->blob_out, io->d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
+  }
+  a.nseg = 1;
+  a.qp = make_qparams(eb);
+  a.st = reinterpret_cast<Status*>(d_status);
+  a.op = op;
+  a.acc_out = acc_out;
+  auto done = [&](int rc) {  // a slotted launch leaves the claim counter at 0 for the next user
+    if (!rc && slotted) rc = (int)cudaMemsetAsync(&wv.hdr->claim, 0, sizeof(unsigned int), (cudaStream_t)stream);
+    return rc;
+  };
+  if (!fused) return done(launch_encode<SRC_PLAIN, 1>(a, ntiles_of(m), (cudaStream_t)stream));
+  a.in_tw = 2.0 * eb;
+  if (io->in_slots) {
+    a.in_slots = io->in_slots;
+    a.in_sizes = io->in_sizes;
+    a.in_w = io->in_widths;
+  } else {
+    SidecarView si = sidecar_view(io->in_sidecar, m);
+    a.in_blob = io->in_blob;
+    a.in_tile_off = si.tile_off;
+    a.in_w = si.widths;
+  }
+  return done(launch_encode<SRC_STEP, 1>(a, ntiles_of(m), (cudaStream_t)stream));
+}
+
+uint64_t gz_slots_bytes(uint64_t m) { return ntiles_of(m) * (uint64_t)TILE_SLOT; }
+
+int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* y,
+                   gz_status* d_status, gz_stream_t stream) {
+  if (!check_eb(eb)) return GZ_EBOUND;
+  if (op != OP_SUM && op != OP_MAX) return GZ_EINVAL;
+  if (!io || !io->in_slots || !io->in_sizes || !io->in_widths || (!y && m) || (!local && m) || !d_status)
+    return GZ_EINVAL;
+  if (m == 0) return 0;
+  DecodeMultiArgs<1> a;
+  std::memset(&a, 0, sizeof(a));
+  a.seg[0] = DecSeg{io->in_slots, nullptr, io->in_widths, m, y, 0, io->in_sizes};
+  a.nseg = 1;
+  a.total_tiles = ntiles_of(m);
+  a.tw = 2.0 * eb;
+  a.local = local;
+  a.op = op;
+  a.st = reinterpret_cast<Status*>(d_status);
+  return launch_decode<1>(a, (cudaStream_t)stream);
 }
 
 int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,

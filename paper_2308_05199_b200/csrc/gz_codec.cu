@@ -50,9 +50,12 @@ struct EncodeArgs {
   const uint8_t* in_blob;  // received blob (header + payload)
   const uint64_t* in_tile_off;
   const uint8_t* in_w;
+  const uint8_t* in_slots; // or: received tiles in slotted form (tile t at t * TILE_SLOT) ...
+  const uint32_t* in_sizes;//     ... with their sizes (in_tile_off unused)
   double in_tw;
   int op;
   float* acc_out;          // optional: reduced values (f32)
+  int slotted_out;         // 1: the output stays in slotted form (scratch/tile_rel), no gather
 };
 
 
@@ -839,12 +842,18 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   auto load_meta = [&](unsigned int jn) {
     InMeta m{0, 0, 0};
     if (SRC == SRC_STEP && jn < total) {
-      m.ts = a.in_tile_off[jn];
-      m.te = a.in_tile_off[jn + 1];
+      if (a.in_slots) {  // slotted input: the tile sits at the start of its slot
+        m.ts = (uint64_t)jn * TILE_SLOT;
+        m.te = m.ts + a.in_sizes[jn];
+      } else {
+        m.ts = a.in_tile_off[jn];
+        m.te = a.in_tile_off[jn + 1];
+      }
       m.w = a.in_w[(uint64_t)jn * TB + lane];
     }
     return m;
   };
+  const uint8_t* const in_base = a.in_slots ? a.in_slots : a.in_blob + HEADER_BYTES;
   unsigned int j = claim();
   unsigned int j1 = j < total ? claim() : total;
   InTile in_cur{0, 0, 0}, in_nxt{0, 0, 0};
@@ -858,7 +867,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     InMeta m_nxt{0, 0, 0};
     if (ONEBUF) {
       m_nxt = load_meta(j1);
-      in_cur.base = stage_bytes<true>(stg0, a.in_blob + HEADER_BYTES, m_cur.ts, m_cur.te, lane);
+      in_cur.base = stage_bytes<true>(stg0, in_base, m_cur.ts, m_cur.te, lane);
       in_cur.bytes = (int)(m_cur.te - m_cur.ts);
       in_cur.w = m_cur.w;
       prefetch_tile(a, j, xsb0, lane, pol_in);  // commits the group
@@ -885,10 +894,12 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
                                                 in_cur.w, s_step, pol_keep, lane);
     if (lane == 0) {
       a.tile_rel[j] = (uint32_t)tb;
-      const uint64_t g = S.gcta_base + (t >> a.gshift);
-      atomicAdd(&a.ws->agg[g], (unsigned)tb);
-      atomicAdd(&a.ws->agg2[g >> 5], (unsigned)tb);
-      atomicAdd(&a.ws->agg3[g >> 10], (unsigned)tb);
+      if (!a.slotted_out) {
+        const uint64_t g = S.gcta_base + (t >> a.gshift);
+        atomicAdd(&a.ws->agg[g], (unsigned)tb);
+        atomicAdd(&a.ws->agg2[g >> 5], (unsigned)tb);
+        atomicAdd(&a.ws->agg3[g >> 10], (unsigned)tb);
+      }
     }
     ++ndone;
     __syncwarp();
@@ -1099,12 +1110,13 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
 // from the owners' memory, in one launch); software pipeline: a tile's bytes
 // and widths are staged one iteration ahead, its offsets two ahead.
 struct DecSeg {
-  const uint8_t* blob;       // header + payload (may be a peer pointer)
+  const uint8_t* blob;       // header + payload (may be a peer pointer); or the slots
   const uint64_t* tile_off;  // sidecar
   const uint8_t* widths;
   uint64_t n;
   float* y;
   uint64_t tile_base;        // first global tile of this blob
+  const uint32_t* sizes;     // slotted input: tile t at blob + t * TILE_SLOT, sizes[t] bytes
 };
 template <int NSEG>
 struct DecodeMultiArgs {
@@ -1152,8 +1164,13 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     if (t < total) {
       const DecSeg& S = a.seg[seg_of(t)];
       const uint64_t lt = t - S.tile_base;
-      m.ts = S.tile_off[lt];
-      m.te = S.tile_off[lt + 1];
+      if (S.sizes) {
+        m.ts = lt * TILE_SLOT;
+        m.te = m.ts + S.sizes[lt];
+      } else {
+        m.ts = S.tile_off[lt];
+        m.te = S.tile_off[lt + 1];
+      }
     }
     return m;
   };
@@ -1163,7 +1180,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     w = 0;
     if (t < total) {
       const DecSeg& S = a.seg[seg_of(t)];
-      base = stage_bytes<true>(stg + bi * STAGE_WORDS, S.blob + HEADER_BYTES, m.ts, m.te, lane);
+      base = stage_bytes<true>(stg + bi * STAGE_WORDS, S.sizes ? S.blob : S.blob + HEADER_BYTES, m.ts, m.te, lane);
       w = S.widths[(t - S.tile_base) * TB + lane];
     }
   };
