@@ -573,8 +573,9 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
     returns its ``counts[rank]`` values — the root its slice verbatim, the
     others their block decoded from the root's compress-once blob.
 
-    * the root compresses all N blocks in virtual-rank order in ONE launch
-      (gz_compress_segments = compress_blocks, codec.py:408-427);
+    * the root compresses the N-1 blocks it sends, in virtual-rank order, in
+      ONE launch (gz_compress_segments = compress_blocks, codec.py:408-427);
+      its own block, kept verbatim, is never sent, so it is not compressed;
     * routing="tree": each rank pulls its subtree's range [vr, vr+extent) of
       blobs + sidecars + lengths from its tree parent in one gz_copy_items
       launch (the reference's byte-range forwarding, collectives.py:511-525),
@@ -643,14 +644,16 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
         lo = [0]
         for c in counts:
             lo.append(lo[-1] + c)
-        xv = x if root == 0 else torch.cat([x[lo[r]:lo[r + 1]] for r in order])
-        arr = ctypes.c_uint64 * N
-        h_counts = arr(*vcounts)
-        ws = self.ws.tile_ws(int(lib.gz_segments_workspace_bytes(h_counts, N)))
+        # the root's own block (virtual rank 0) is never sent (root_sends cover
+        # [1, N), collectives.py:503-508): only blocks 1..N-1 are compressed
+        xv = x[lo[1]:] if root == 0 else torch.cat([x[lo[r]:lo[r + 1]] for r in order[1:]])
+        arr = ctypes.c_uint64 * (N - 1)
+        h_counts = arr(*vcounts[1:])
+        ws = self.ws.tile_ws(int(lib.gz_segments_workspace_bytes(h_counts, N - 1)))
         base = self._sc_buf.data_ptr()
-        L.check(lib.gz_compress_segments(xv.data_ptr(), h_counts, N, ebf, base, arr(*lay.slot), base + lay.len_off,
-                                         base, arr(*lay.sc), ws.data_ptr(), ws.numel(), self.ws.status_ptr(), s),
-                "gz_compress_segments")
+        L.check(lib.gz_compress_segments(xv.data_ptr(), h_counts, N - 1, ebf, base, arr(*lay.slot[1:]),
+                                         base + lay.len_off + 8, base, arr(*lay.sc[1:]), ws.data_ptr(), ws.numel(),
+                                         self.ws.status_ptr(), s), "gz_compress_segments")
         out.copy_(x[lo[me]:lo[me + 1]])
         launches += 2 + (root != 0)
         targets = [c for c, _, _ in sends] if routing == "tree" else [j for j in range(N) if j != me]
