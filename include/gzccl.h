@@ -133,7 +133,7 @@ uint64_t gz_slots_bytes(uint64_t m);
 int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,
             uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream);
 /* y = op(local, decode(slotted input io->in_*)): a reduce-scatter's last step
- * without re-compression (collectives.py:285-290) */
+ * without re-compression (collectives.py:285-290); local == NULL: y = decode(...) */
 int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* y,
                    gz_status* d_status, gz_stream_t stream);
 

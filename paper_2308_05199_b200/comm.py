@@ -697,23 +697,25 @@ Communicator.binomial_scatter = binomial_scatter
 
 
 class _RDLayout:
-    """Recursive doubling: one worst-case slot (blob + sidecar) per message a
-    rank can receive -- 0: the donor's buffer (absorbers), 1..steps: the
-    exchange steps, steps+1: the absorber's final result (donors) -- plus
-    full[k] / consumed[k] flags and the blob lengths."""
+    """Recursive doubling: one slotted message buffer per message a rank can
+    SEND -- 0: the donor's buffer (donors), 1..steps: the exchange steps,
+    steps+1: the absorber's final result (absorbers) -- read in place by the
+    receiving peer over NVLink; plus full[k] / consumed[k] flags."""
 
     def __init__(self, n: int, steps: int):
         lib = L.lib()
         self.K = steps + 2
+        nt = int(lib.gz_num_tiles(n))
         off = _al(4 * 2 * self.K)
-        self.len_off = off
-        off += _al(8 * self.K)
-        self.cap = _al(int(lib.gz_compress_bound(n)))
-        self.scb = int(lib.gz_sidecar_bytes(n))
         self.slot = []
         for _ in range(self.K):
-            self.slot.append((off, off + self.cap))
-            off += self.cap + _al(self.scb)
+            sl = off
+            off += _al(int(lib.gz_slots_bytes(n)))
+            sz = off
+            off += _al(4 * nt)
+            wd = off
+            off += _al(32 * nt)
+            self.slot.append((sl, sz, wd))
         self.total = off
 
     def full(self, k):
@@ -726,13 +728,14 @@ class _RDLayout:
 def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
     """This rank's part of rd_allreduce_c (collectives.py:349-424) over NVLink.
 
-    Whole-buffer exchanges with the partner actual(remapped(i) ^ 2^t); every
-    reduction followed by a send is one fused kernel that updates the buffer
-    in place and stores compress(buffer) straight into the partner's slot;
-    the last reduction of a non-absorber is gz_decompress_reduce.  Donors
-    (even ranks below 2r) fold into their absorber first and receive the
-    result compressed at the end.  Outputs are per rank, bit-exact with the
-    reference.
+    Whole-buffer exchanges with the partner actual(remapped(i) ^ 2^t).  Every
+    message stays in the sender's memory in slotted form and the receiver's
+    kernel reads it in place (pull); every reduction followed by a send is one
+    fused kernel (decode the partner's message + op + compress), the last
+    reduction of a non-absorber a decode+op kernel.  The input buffer is only
+    read: the first reduction writes `out`.  Donors (even ranks below 2r) fold
+    into their absorber first and receive the result compressed at the end.
+    Outputs are per rank, bit-exact with the reference.
     """
     from .collectives import rd_plan
 
@@ -742,8 +745,8 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
     N, i = self.world, self.rank
     if out is None:
         out = torch.empty_like(x)
-    out.copy_(x)
     if N == 1:
+        out.copy_(x)
         return out
     n = x.numel()
     pof2, r, steps, role, remapped, actual = rd_plan(N)
@@ -764,6 +767,7 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
     tws = ws.tile_ws(int(lib.gz_workspace_bytes(n)))
     K = lay.K
     launches = 0
+    data = [x.data_ptr()]  # the current buffer: x until the first reduction writes out
 
     def at(rr, off):
         return peer[rr] + off
@@ -775,56 +779,56 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
     def signal(rr, off):
         L.check(lib.gz_stream_write_u32(s, at(rr, off), e), "gz_stream_write_u32")
 
-    def dest(rr, k):  # blob, length word, sidecar of rank rr's slot k
-        b, sc = lay.slot[k]
-        return at(rr, b), at(rr, lay.len_off + 8 * k), at(rr, sc)
+    def msg(rr, k):  # (slots, sizes, widths) of the message rank rr sends as number k
+        return tuple(at(rr, o) for o in lay.slot[k])
 
-    def compress_to(rr, k):
+    def send(k, rr, src=None, k_in=None):
+        """message k to rr: compress(data) or, with (src, k_in), the fused
+        out = op(data, dec(src's message k_in)); compress(out)"""
         nonlocal launches
-        wait(lay.consumed(k), prev)  # rr consumed what we wrote there last call
-        b, ln, sc = dest(rr, k)
-        L.check(lib.gz_compress(out.data_ptr(), n, ebf, 32, b, lay.cap, ln, sc, None, tws.data_ptr(), tws.numel(),
-                                ws.status_ptr(), s), "gz_compress")
-        launches += 2
+        wait(lay.consumed(k), prev)  # rr consumed our message k of the previous call
+        io = _StepIO()
+        io.out_slots, io.out_sizes, io.out_widths = msg(i, k)
+        acc = None
+        if src is not None:
+            io.in_slots, io.in_sizes, io.in_widths = msg(src, k_in)
+            acc = out.data_ptr()
+        L.check(lib.gz_step(ctypes.byref(io), data[0], n, ebf, opc, acc, tws.data_ptr(), tws.numel(),
+                            ws.status_ptr(), s), "gz_step")
+        launches += 1
+        data[0] = out.data_ptr() if acc is not None else data[0]
         signal(rr, lay.full(k))
 
-    def fused_to(k_in, rr, k):  # out = op(out, dec(my slot k_in)); compress(out) -> rr's slot k
+    def receive_last(src, k_in, reduce: bool):  # out = [op(data,] dec(src's message k_in)[)]
         nonlocal launches
-        wait(lay.consumed(k), prev)
-        b, ln, sc = dest(rr, k)
-        ib, _, isc = dest(i, k_in)
-        L.check(lib.gz_reduce_step(ib, isc, out.data_ptr(), n, ebf, opc, out.data_ptr(), b, lay.cap, ln, sc,
-                                   tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_reduce_step")
-        launches += 2
-        signal(rr, lay.full(k))
+        io = _StepIO()
+        io.in_slots, io.in_sizes, io.in_widths = msg(src, k_in)
+        L.check(lib.gz_step_reduce(ctypes.byref(io), data[0] if reduce else None, n, ebf, opc, out.data_ptr(),
+                                   ws.status_ptr(), s), "gz_step_reduce")
+        launches += 1
 
     if role(i) == "donor":
         a = i + 1
-        compress_to(a, 0)  # 381-386
+        send(0, a)  # 381-386
         wait(lay.full(K - 1), e)  # 430-435: the absorber's result
-        b, _, sc = dest(i, K - 1)
-        L.check(lib.gz_decompress_sidecar(b, sc, n, ebf, out.data_ptr(), ws.status_ptr(), s), "gz_decompress_sidecar")
-        launches += 1
+        receive_last(a, K - 1, reduce=False)
         signal(a, lay.consumed(K - 1))
     else:
         part = [actual(remapped(i) ^ (1 << t)) for t in range(steps)]
         if role(i) == "absorber":
             wait(lay.full(0), e)  # 389-397, fused with the step-0 compression
-            fused_to(0, part[0], 1)
+            send(1, part[0], src=i - 1, k_in=0)
             signal(i - 1, lay.consumed(0))
         else:
-            compress_to(part[0], 1)
+            send(1, part[0])
         for t in range(steps):  # 399-418
             wait(lay.full(t + 1), e)
             if t + 1 < steps:
-                fused_to(t + 1, part[t + 1], t + 2)
+                send(t + 2, part[t + 1], src=part[t], k_in=t + 1)
             elif role(i) == "absorber":
-                fused_to(t + 1, i - 1, K - 1)  # 420-427: the result goes back to the donor
+                send(K - 1, i - 1, src=part[t], k_in=t + 1)  # 420-427: the result goes back to the donor
             else:
-                ib, _, isc = dest(i, t + 1)
-                L.check(lib.gz_decompress_reduce(ib, isc, out.data_ptr(), n, ebf, opc, out.data_ptr(), ws.status_ptr(),
-                                                 s), "gz_decompress_reduce")
-                launches += 1
+                receive_last(part[t], t + 1, reduce=True)
             signal(part[t], lay.consumed(t + 1))
     self._rd_epoch = e
     self.launches_per_call = launches

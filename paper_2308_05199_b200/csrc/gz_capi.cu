@@ -566,8 +566,7 @@ int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double 
                    gz_status* d_status, gz_stream_t stream) {
   if (!check_eb(eb)) return GZ_EBOUND;
   if (op != OP_SUM && op != OP_MAX) return GZ_EINVAL;
-  if (!io || !io->in_slots || !io->in_sizes || !io->in_widths || (!y && m) || (!local && m) || !d_status)
-    return GZ_EINVAL;
+  if (!io || !io->in_slots || !io->in_sizes || !io->in_widths || (!y && m) || !d_status) return GZ_EINVAL;
   if (m == 0) return 0;
   DecodeMultiArgs<1> a;
   std::memset(&a, 0, sizeof(a));
