@@ -59,17 +59,13 @@ struct EncodeArgs {
 };
 
 
-// Fused step: the received tile's bytes are staged synchronously and the
-// local values are loaded for the current tile only (one value buffer, one
-// staging buffer per warp): 24 warps per SM hide the latency better than
-// 16 double-buffered or 13 fully asynchronous warps (measured).
-constexpr bool STEP_ASYNC_STAGE = false;
-constexpr int STEP_BUFS = 1;
-constexpr int ENC_WARP_SMEM = STEP_BUFS * TILE_VALUES * 4 + (STEP_ASYNC_STAGE ? 2 : 1) * STAGE_BYTES;
+// Fused step: the local values are loaded for the current tile only and the
+// received tile's bytes staged alongside (one value buffer, one staging
+// buffer per warp): 24 warps per SM hide the latency better than 16
+// double-buffered or 13 fully asynchronous warps (measured, profiles/).
+constexpr int ENC_WARP_SMEM = TILE_VALUES * 4 + STAGE_BYTES;
 // warps per encoder CTA (one CTA per SM): as many as shared memory allows
-__host__ __device__ constexpr int enc_warps(int src) {
-  return src == 1 ? (STEP_ASYNC_STAGE ? 13 : (STEP_BUFS == 2 ? 16 : 24)) : 24;
-}
+__host__ __device__ constexpr int enc_warps(int src) { return 24; }
 
 // -------------------------------------------------------------------------
 // small helpers
@@ -104,28 +100,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Warp-synchronous fill of the swizzled tile xs[32][32] with src[v0, v0+nval):
-// asynchronous (cp.async) for a full 16-byte aligned tile, direct otherwise.
-// Always commits exactly one cp.async group.
-__device__ __forceinline__ void prefetch_values(float* xs, const float* __restrict__ src, uint64_t v0, int nval, int lane) {
-  const float* p = src + v0;
-  if (nval == TILE_VALUES && ((reinterpret_cast<uintptr_t>(p) & 15) == 0)) {
-    const float4* p4 = reinterpret_cast<const float4*>(p);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int i = lane + 32 * j;
-      cp_async16(xs + xs_index(i >> 3, i & 7), p4 + i);
-    }
-  } else if (nval > 0) {
-    for (int i = lane; i < TILE_VALUES; i += 32) {
-      const float v = i < nval ? __ldcs(p + i) : 0.0f;
-      const int row = i >> 5, col = i & 31;
-      xs[xs_index(row, col >> 2) + (col & 3)] = v;
-    }
-  }
-  cp_async_commit();
-}
 
 // Warp-synchronous coalesced write of the tile to dst[v0, v0+nval).
 __device__ __forceinline__ void drain_values(const float* xs, float* __restrict__ dst, uint64_t v0, int nval, int lane) {
@@ -312,76 +286,6 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v)
   return v;
 }
 
-// -------------------------------------------------------------------------
-// Copy `len` bytes from 16-byte aligned src to arbitrary dst (dst may be a
-// peer GPU's memory): aligned 16-byte stores in the middle, byte stores at
-// the two ragged ends.  Warp-cooperative.
-__device__ __forceinline__ void copy_to_unaligned(uint8_t* dst, const uint8_t* src, uint64_t len, int lane) {
-  if (!len) return;
-  const uintptr_t A = reinterpret_cast<uintptr_t>(dst);
-  const uintptr_t E = A + len;
-  const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cl = E & ~(uintptr_t)15;
-  const uint32_t* sw = reinterpret_cast<const uint32_t*>(src);
-  if (cf < cl) {
-    const uint64_t off0 = cf - A;  // source byte of the first full destination chunk
-    const int sh = (int)(off0 & 3) * 8;
-    const uint64_t nch = (cl - cf) >> 4;
-    uint4* d = reinterpret_cast<uint4*>(cf);
-    for (uint64_t c = lane; c < nch; c += 32) {
-      const uint64_t wi = (off0 >> 2) + 4 * c;
-      const uint32_t w0 = __ldcg(sw + wi), w1 = __ldcg(sw + wi + 1), w2 = __ldcg(sw + wi + 2), w3 = __ldcg(sw + wi + 3),
-                     w4 = __ldcg(sw + wi + 4);
-      uint4 v;
-      v.x = __funnelshift_r(w0, w1, sh);
-      v.y = __funnelshift_r(w1, w2, sh);
-      v.z = __funnelshift_r(w2, w3, sh);
-      v.w = __funnelshift_r(w3, w4, sh);
-      d[c] = v;
-    }
-    const int head = (int)(cf - A), tail = (int)(E - cl);
-    if (lane < head) dst[lane] = src[lane];
-    if (lane >= 16 && lane - 16 < tail) dst[len - tail + (lane - 16)] = src[len - tail + (lane - 16)];
-  } else {
-    for (uint64_t i = lane; i < len; i += 32) dst[i] = src[i];
-  }
-}
-
-// One thread copies `len` bytes from a 16-byte aligned slot to an arbitrary
-// destination (possibly a peer GPU): byte stores up to the first 16-byte
-// boundary, aligned 16-byte stores (source re-aligned with funnel shifts),
-// byte stores for the tail.  Neighbouring tiles only share the edge chunks,
-// which are written byte-wise, so concurrent lanes never overlap.
-__device__ __forceinline__ void lane_copy(uint8_t* dst, const uint8_t* src, int len) {
-  if (len <= 0) return;
-  const int h = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
-  for (int i = 0; i < h; ++i) dst[i] = src[i];
-  const int nch = (len - h) >> 4;
-  if (nch > 0) {
-    const uint4* s4 = reinterpret_cast<const uint4*>(src + (h & ~15));
-    uint4* d4 = reinterpret_cast<uint4*>(dst + h);
-    const int wo = (h >> 2) & 3, sh = (h & 3) * 8;
-    uint4 cur = __ldcg(s4);
-#pragma unroll 2
-    for (int c = 0; c < nch; ++c) {
-      const uint4 nxt = __ldcg(s4 + c + 1);
-      // words wo..wo+4 of the 8-word window (cur, nxt)
-      const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-      const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-      const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-      const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-      const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-      uint4 o;
-      o.x = __funnelshift_r(a0, a1, sh);
-      o.y = __funnelshift_r(a1, a2, sh);
-      o.z = __funnelshift_r(a2, a3, sh);
-      o.w = __funnelshift_r(a3, a4, sh);
-      d4[c] = o;
-      cur = nxt;
-    }
-  }
-  for (int i = h + 16 * nch; i < len; ++i) dst[i] = src[i];
-}
-
 struct SegGeom {
   uint64_t n, nb, ntiles;
   int last_cnt;
@@ -417,13 +321,6 @@ __device__ __forceinline__ uint64_t pol_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
-}
-__device__ __forceinline__ void cp_async16_hint(void* sdst, const void* gsrc, uint64_t pol) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(sdst);
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(s), "l"(gsrc), "l"(pol) : "memory");
-}
-__device__ __forceinline__ void discard_l2_line(const void* p) {
-  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
 // Start loading tile `t` (global tile index) into xs (evict-first: the values
@@ -621,150 +518,6 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   return tile_bytes;
 }
 
-// Warp-cooperative copy of `len` bytes from 16-byte aligned `src` to any
-// `dst` (possibly a peer GPU): each lane produces whole aligned 16-byte
-// destination chunks from two source chunks; loads are batched so that
-// several round trips are in flight per lane.  Edge bytes are written
-// byte-wise (shared with neighbouring ranges).
-__device__ __forceinline__ void copy_run(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, uint64_t len, int lane) {
-  if (!len) return;
-  const uintptr_t A = reinterpret_cast<uintptr_t>(dst), E = A + len;
-  const uintptr_t cf = (A + 15) & ~(uintptr_t)15, cl = E & ~(uintptr_t)15;
-  if (cf >= cl) {
-    for (uint64_t i = lane; i < len; i += 32) dst[i] = src[i];
-    return;
-  }
-  const uint64_t head = cf - A, nch = (cl - cf) >> 4;
-  const int sh = (int)(head & 3) * 8, wo = (int)(head >> 2) & 3;
-  const uint4* s4 = reinterpret_cast<const uint4*>(src + (head & ~(uint64_t)15));
-  uint4* d4 = reinterpret_cast<uint4*>(cf);
-  constexpr int B = 4;
-  for (uint64_t c0 = lane; c0 < nch; c0 += 32 * B) {
-    uint4 lo[B], hi[B];
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const uint64_t c = c0 + 32 * b;
-      if (c < nch) {
-        lo[b] = __ldcs(s4 + c);
-        hi[b] = __ldcs(s4 + c + 1);
-      }
-    }
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      const uint64_t c = c0 + 32 * b;
-      if (c < nch) {
-        const uint4 cur = lo[b], nxt = hi[b];
-        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-        uint4 o;
-        o.x = __funnelshift_r(a0, a1, sh);
-        o.y = __funnelshift_r(a1, a2, sh);
-        o.z = __funnelshift_r(a2, a3, sh);
-        o.w = __funnelshift_r(a3, a4, sh);
-        d4[c] = o;
-      }
-    }
-  }
-  const int tail = (int)(E - cl);
-  if ((uint64_t)lane < head) dst[lane] = src[lane];
-  if (lane >= 16 && lane - 16 < tail) dst[len - tail + (lane - 16)] = src[len - tail + (lane - 16)];
-}
-
-// Lane-per-tile copy with batched loads: `len` bytes from a 16-byte aligned
-// slot to any destination (possibly a peer GPU); byte stores for the ragged
-// edges (shared with neighbouring tiles, hence byte-wise), aligned 16-byte
-// stores in between, eight source chunks in flight per batch.
-__device__ __forceinline__ void lane_copy_batched(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src, int len) {
-  if (len <= 0) return;
-  const int h = min(len, (int)((16 - (reinterpret_cast<uintptr_t>(dst) & 15)) & 15));
-  for (int i = 0; i < h; ++i) dst[i] = src[i];
-  const int nch = (len - h) >> 4;
-  const uint4* s4 = reinterpret_cast<const uint4*>(src + (h & ~15));
-  uint4* d4 = reinterpret_cast<uint4*>(dst + h);
-  const int wo = (h >> 2) & 3, sh = (h & 3) * 8;
-  constexpr int B = 8;
-  for (int c0 = 0; c0 < nch; c0 += B) {
-    uint4 v[B + 1];
-#pragma unroll
-    for (int b = 0; b <= B; ++b)
-      if (c0 + b <= nch) v[b] = __ldcs(s4 + c0 + b);
-#pragma unroll
-    for (int b = 0; b < B; ++b) {
-      if (c0 + b < nch) {
-        const uint4 cur = v[b], nxt = v[b + 1];
-        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-        uint4 o;
-        o.x = __funnelshift_r(a0, a1, sh);
-        o.y = __funnelshift_r(a1, a2, sh);
-        o.z = __funnelshift_r(a2, a3, sh);
-        o.w = __funnelshift_r(a3, a4, sh);
-        d4[c0 + b] = o;
-      }
-    }
-  }
-  for (int i = h + 16 * nch; i < len; ++i) dst[i] = src[i];
-}
-
-// Warp-cooperative copy of up to 4 tiles at once (coalesced): tile i has
-// `len[i]` bytes in a 16-byte aligned slot `src[i]` and goes to `dst[i]`
-// (any alignment, possibly a peer GPU).  Lane l produces aligned destination
-// chunk l (+32, +64, ... for long tiles) from source chunks l and l+1; all
-// loads of the group are issued before the stores.  Edge bytes are written
-// byte-wise (they share 16-byte chunks with neighbouring tiles).
-__device__ __forceinline__ void warp_copy4(uint8_t* const (&dst)[4], const uint8_t* const (&src)[4], const int (&len)[4],
-                                           int lane) {
-  int head[4], nch[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    head[i] = min(len[i], (int)((16 - (reinterpret_cast<uintptr_t>(dst[i]) & 15)) & 15));
-    nch[i] = len[i] > head[i] ? (len[i] - head[i]) >> 4 : 0;
-  }
-  const int maxch = max(max(nch[0], nch[1]), max(nch[2], nch[3]));
-  for (int c0 = 0; c0 < maxch; c0 += 32) {
-    const int cc = c0 + lane;
-    uint4 lo[4], hi[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (cc < nch[i]) {
-        const uint4* s4 = reinterpret_cast<const uint4*>(src[i] + (head[i] & ~15));
-        lo[i] = __ldcs(s4 + cc);
-        hi[i] = __ldcs(s4 + cc + 1);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (cc < nch[i]) {
-        const int h = head[i], wo = (h >> 2) & 3, sh = (h & 3) * 8;
-        const uint4 cur = lo[i], nxt = hi[i];
-        const uint32_t a0 = wo == 0 ? cur.x : wo == 1 ? cur.y : wo == 2 ? cur.z : cur.w;
-        const uint32_t a1 = wo == 0 ? cur.y : wo == 1 ? cur.z : wo == 2 ? cur.w : nxt.x;
-        const uint32_t a2 = wo == 0 ? cur.z : wo == 1 ? cur.w : wo == 2 ? nxt.x : nxt.y;
-        const uint32_t a3 = wo == 0 ? cur.w : wo == 1 ? nxt.x : wo == 2 ? nxt.y : nxt.z;
-        const uint32_t a4 = wo == 0 ? nxt.x : wo == 1 ? nxt.y : wo == 2 ? nxt.z : nxt.w;
-        uint4 o;
-        o.x = __funnelshift_r(a0, a1, sh);
-        o.y = __funnelshift_r(a1, a2, sh);
-        o.z = __funnelshift_r(a2, a3, sh);
-        o.w = __funnelshift_r(a3, a4, sh);
-        reinterpret_cast<uint4*>(dst[i] + h)[cc] = o;
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int tail0 = head[i] + 16 * nch[i];
-    if (lane < head[i]) dst[i][lane] = src[i][lane];
-    for (int b = tail0 + lane; b < len[i]; b += 32) dst[i][b] = src[i][b];
-  }
-}
-
 // Encoder, kernel 1 of 2 (one CTA per SM, no CTA-wide barrier after setup).
 // CTA c owns a contiguous tile range of one segment (CTAs are split over
 // segments in proportion to their tiles).  Its warps claim tiles of the range
@@ -787,10 +540,9 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   constexpr int WSMEM = SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4;
   unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
-  constexpr bool ONEBUF = SRC == SRC_STEP && STEP_BUFS == 1;
+  constexpr bool ONEBUF = SRC == SRC_STEP;  // the fused step: one value buffer + one staging buffer
   float* xsb1 = ONEBUF ? xsb0 : reinterpret_cast<float*>(my + TILE_VALUES * 4);
-  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + (ONEBUF ? 1 : 2) * TILE_VALUES * 4);  // fused step only
-  uint32_t* stg1 = STEP_ASYNC_STAGE ? stg0 + STAGE_WORDS : stg0;
+  uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4);  // fused step only
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
   if (tid == 0) s_next = 0;
   __syncthreads();
@@ -817,20 +569,8 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     }
     return __shfl_sync(0xFFFFFFFFu, v, 0);
   };
-  // fused step: the received blob's tile jn is staged with the local values
-  // (same cp.async group); its offsets come from the sidecar
   struct InTile {
     int base, bytes, w;
-  };
-  auto stage_in = [&](unsigned int jn, uint32_t* stg) {
-    InTile r{0, 0, 0};
-    if (SRC == SRC_STEP && jn < total) {
-      const uint64_t ts = a.in_tile_off[jn], te = a.in_tile_off[jn + 1];
-      r.base = stage_bytes<STEP_ASYNC_STAGE>(stg, a.in_blob + HEADER_BYTES, ts, te, lane);
-      r.bytes = (int)(te - ts);
-      r.w = a.in_w[(uint64_t)jn * TB + lane];  // (the sidecar has a full tile of widths)
-    }
-    return r;
   };
   // fused step, one buffer: the received tile's sidecar entries (offsets,
   // widths) are loaded one tile ahead; its bytes and the local values are
@@ -856,9 +596,8 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   const uint8_t* const in_base = a.in_slots ? a.in_slots : a.in_blob + HEADER_BYTES;
   unsigned int j = claim();
   unsigned int j1 = j < total ? claim() : total;
-  InTile in_cur{0, 0, 0}, in_nxt{0, 0, 0};
+  InTile in_cur{0, 0, 0};
   InMeta m_cur = ONEBUF ? load_meta(j) : InMeta{0, 0, 0};
-  if (STEP_ASYNC_STAGE) in_cur = stage_in(j, stg0);
   if (j < total && !ONEBUF) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
   unsigned long long wait_ns = 0, ndone = 0;
@@ -873,15 +612,10 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
       prefetch_tile(a, j, xsb0, lane, pol_in);  // commits the group
       cp_async_wait_all();
       __syncwarp();
-    } else {
-      if (STEP_ASYNC_STAGE) in_nxt = stage_in(j1, buf ? stg0 : stg1);
+    } else {  // plain compression: the next tile is prefetched while this one is encoded
       prefetch_tile(a, j1, buf ? xsb0 : xsb1, lane, pol_in);
       cp_async_wait_1();
       __syncwarp();
-      if (SRC == SRC_STEP && !STEP_ASYNC_STAGE) {
-        in_cur = stage_in(j, stg0);
-        __syncwarp();
-      }
     }
     const int k = NSEG > 1 ? seg_of_tile(a, j) : 0;
     const Seg& S = a.seg[k];
@@ -889,9 +623,8 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     const uint64_t t = j - S.tile_base;
     const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
                                                 reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), 0,
-                                                false, dummy, (STEP_ASYNC_STAGE && buf) ? stg1 : stg0, in_cur.base,
-                                                in_cur.bytes,
-                                                in_cur.w, s_step, pol_keep, lane);
+                                                false, dummy, stg0, in_cur.base, in_cur.bytes, in_cur.w, s_step,
+                                                pol_keep, lane);
     if (lane == 0) {
       a.tile_rel[j] = (uint32_t)tb;
       if (!a.slotted_out) {
@@ -905,7 +638,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     __syncwarp();
     buf ^= 1;
     j = j1;
-    in_cur = in_nxt;
     m_cur = m_nxt;
     j1 = j < total ? claim() : total;
   }
