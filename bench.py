@@ -147,7 +147,7 @@ def run_reference(args):
         n = 1 << 21  # 8 MiB per rank
         bufs = [O.smooth_field(n, 0.37 * r) for r in range(N)]
         t0 = time.perf_counter()
-        O.ring_allreduce(bufs, EB)
+        O.ring_allreduce(bufs, EB, threads=threads)
         dt = time.perf_counter() - t0
         gbs = 4 * n / dt / 1e9
         line = {"metric": METRIC, "value": round(gbs, 5), "unit": "GB/s", "n_gpus": N, "steps": 1,
@@ -155,7 +155,7 @@ def run_reference(args):
                 "vs_baseline": None, "dtype": "f32->u8 (f64 closed loop)", "data": "synthetic smooth field",
                 "impl": "reference",
                 "config": {"workload": f"ring-allreduce eb=1e-4, N={N} virtual ranks on the host, 8 MiB per rank sample"},
-                "cpu_baseline": {"value": round(gbs, 5), "unit": "GB/s", "cores": 1, "kind": "port",
+                "cpu_baseline": {"value": round(gbs, 5), "unit": "GB/s", "cores": threads, "kind": "port",
                                  "sample": "8 MiB per rank (bounded sample of the 512 MiB workload)"},
                 "e2e": {"value": round(gbs, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -132,10 +132,10 @@ class Trace:
     msgs: list
 
 
-def ring_reduce_scatter(bufs, eb, op="sum", trace=None, raw=False):
+def ring_reduce_scatter(bufs, eb, op="sum", trace=None, raw=False, threads=1):
     """ring_reduce_scatter_c, collectives.py:258-291 (two-pass schedule)."""
-    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb))
-    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else decompress
+    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb, threads=threads))
+    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else (lambda b: decompress(b, threads=threads))
     bufs = [np.ascontiguousarray(b, "<f4") for b in bufs]
     N = len(bufs)
     n = bufs[0].size
@@ -157,10 +157,10 @@ def ring_reduce_scatter(bufs, eb, op="sum", trace=None, raw=False):
     return [acc[i][(i + 1) % N] for i in range(N)]
 
 
-def ring_allgather_owned(owned, eb, chunk_of, trace=None, raw=False):
+def ring_allgather_owned(owned, eb, chunk_of, trace=None, raw=False, threads=1):
     """_ring_allgather, collectives.py:215-244: compress once, forward bytes."""
-    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb))
-    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else decompress
+    enc = (lambda a: np.ascontiguousarray(a, "<f4").tobytes()) if raw else (lambda a: compress(a, eb, threads=threads))
+    dec = (lambda b: np.frombuffer(b, "<f4").copy()) if raw else (lambda b: decompress(b, threads=threads))
     N = len(owned)
     gathered = [{chunk_of(i): owned[i]} for i in range(N)]
     if N == 1:
@@ -177,14 +177,14 @@ def ring_allgather_owned(owned, eb, chunk_of, trace=None, raw=False):
     return gathered
 
 
-def ring_allreduce(bufs, eb, op="sum", trace=None, raw=False):
-    """ring_allreduce_c, collectives.py:294-308."""
+def ring_allreduce(bufs, eb, op="sum", trace=None, raw=False, threads=1):
+    """ring_allreduce_c, collectives.py:294-308 (threads: host threads per codec call)."""
     bufs = [np.ascontiguousarray(b, "<f4") for b in bufs]
     N = len(bufs)
     if N == 1:
         return [bufs[0].copy()]
-    owned = ring_reduce_scatter(bufs, eb, op, trace, raw)
-    gathered = ring_allgather_owned(owned, eb, lambda i: (i + 1) % N, trace, raw)
+    owned = ring_reduce_scatter(bufs, eb, op, trace, raw, threads)
+    gathered = ring_allgather_owned(owned, eb, lambda i: (i + 1) % N, trace, raw, threads)
     return [np.concatenate([gathered[i][c] for c in range(N)]) for i in range(N)]
 
 
