@@ -128,6 +128,8 @@ typedef struct {
   uint8_t* out_slots;
   uint32_t* out_sizes;
   uint8_t* out_widths;
+  uint32_t* post_flag; /* slotted output only, may be NULL: the kernel stores 1 here (e.g. a peer's flag,
+                          IPC-mapped) once the whole output is written -- a fused gz_stream_write_u32 */
 } gz_step_io;
 uint64_t gz_slots_bytes(uint64_t m);
 int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,
@@ -155,6 +157,15 @@ int gz_enable_peer_access(int peer_device);
 /* stream-ordered flags (driver stream memory ops; no spinning kernels) */
 int gz_stream_write_u32(gz_stream_t stream, void* dptr, uint32_t value);
 int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value);
+/* several flag operations as ONE stream memory-op batch (one graph node),
+ * executed in array order: kind 0 = write value, kind 1 = wait until >= value */
+typedef struct {
+  void* ptr;
+  uint32_t value;
+  uint32_t kind;
+} gz_flag_op;
+#define GZ_MAX_FLAG_OPS 64
+int gz_stream_flag_ops(gz_stream_t stream, const gz_flag_op* ops, uint32_t count);
 /* copy `*d_len + tail` bytes determined on the device: dst may be a peer */
 int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64_t max_bytes, gz_stream_t stream);
 
@@ -187,6 +198,9 @@ int gz_fr_decompress(const uint8_t* blob, uint64_t n, uint32_t bits, float* y, g
 
 /* number of kernels this library has launched so far (all entry points) */
 uint64_t gz_launch_count(void);
+/* profiling only: stream-ordered write of the GPU's %globaltimer (ns, u64) into dst;
+ * works inside a captured CUDA graph (tools/prof_ring_stamps.py) */
+int gz_debug_stamp(void* dst, gz_stream_t stream);
 
 #ifdef __cplusplus
 }

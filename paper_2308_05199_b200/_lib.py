@@ -44,10 +44,12 @@ SIGNATURES = {
     "gz_enable_peer_access": (i32, [i32]),
     "gz_stream_write_u32": (i32, [p, p, u32]),
     "gz_stream_wait_u32_geq": (i32, [p, p, u32]),
+    "gz_stream_flag_ops": (i32, [p, p, u32]),
     "gz_copy_blob": (i32, [p, p, p, u64, p]),
     "gz_copy_items": (i32, [p, u32, p]),
     "gz_copy_items_sms": (i32, [p, u32, i32, p]),
     "gz_launch_count": (u64, []),
+    "gz_debug_stamp": (i32, [p, p]),
     "gz_slots_bytes": (u64, [u64]),
     "gz_step": (i32, [p, p, u64, dbl, i32, p, p, u64, p, p]),
     "gz_step_reduce": (i32, [p, p, u64, dbl, i32, p, p, p]),

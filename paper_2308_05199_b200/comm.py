@@ -42,6 +42,7 @@ from .schedule import Compress, Reduce, ring_allreduce_plan
 
 _ALIGN = 256
 AG_COPY_SMS = 24  # SMs left to the allgather's NVLink pulls while the previous owner's blob is decoded
+AG_MULTI_MAX = 8 << 20  # chunk values up to which the allgather decodes every owner in one remote-read launch
 
 
 def _al(v: int) -> int:
@@ -117,13 +118,18 @@ class Communicator:
         self.last_compression_ratio = None
         self.launches_per_call = 0
         self.events = None  # list -> (label, cuda event) marks after every wait/launch (profiling)
+        self.stamps = None  # int64 device tensor -> %globaltimer stamps at the same marks (profiling)
+        self.stamp_labels = []
         self.copy_stream = torch.cuda.Stream(self.device)  # allgather pulls
         self.use_graphs = True  # replay repeated ring calls from a captured CUDA graph
         self.graph_launches = 0  # kernels executed by graph replays (not seen by gz_launch_count)
         self.capture_stream = torch.cuda.Stream(self.device)
         self._graph_cache = {}
         self._last_key = None
-        self.ag_mode = "copy"  # allgather: "multi" (one remote-read decode launch) or "copy" (pull, then local decode)
+        # allgather: "multi" (one launch decodes every owner's blob out of its memory), "copy" (pull each
+        # blob over NVLink on a side stream, decode it locally) or "auto" (multi for chunks up to
+        # AG_MULTI_MAX values, where it wins by up to ~30 µs per call at N = 4; copy above)
+        self.ag_mode = "auto"
 
     # ------------------------------------------------------------------ setup
     def _setup(self, m_max: int):
@@ -207,10 +213,31 @@ class Communicator:
         self._signal(r, off, 1, s)
 
     def _take(self, off: int, s: int):
-        self._wait(off, 1, s)
-        self._signal(self.rank, off, 0, s)
+        self._take_all([off], s)
+
+    def _flag_ops(self, ops, s: int):
+        """ops: [(kind, addr, value)], kind 0 = write, 1 = wait >= value; one
+        stream memory-op batch (a single graph node)."""
+        arr = (_FlagOp * len(ops))(*[_FlagOp(a, v, k) for k, a, v in ops])
+        L.check(L.lib().gz_stream_flag_ops(s, arr, len(ops)), "gz_stream_flag_ops")
+
+    def _take_all(self, offs, s: int, mark: bool = True):
+        """take several of our own flags: wait for all, then reset all (one batch)"""
+        mine = [self._addr(self.rank, off) for off in offs]
+        self._flag_ops([(1, a, 1) for a in mine] + [(0, a, 0) for a in mine], s)
+        if mark:
+            self._mark("wait")
+
+    def _post_all(self, targets, s: int):
+        """post flags in several peers' memory: [(rank, off)] (one batch)"""
+        self._flag_ops([(0, self._addr(r, off), 1) for r, off in targets], s)
 
     def _mark(self, label: str):
+        if self.stamps is not None:  # profiling: device timestamps, also inside a captured graph
+            k = len(self.stamp_labels)
+            if k < self.stamps.numel():
+                self.stamp_labels.append(label)
+                L.lib().gz_debug_stamp(self.stamps.data_ptr() + 8 * k, torch.cuda.current_stream(self.device).cuda_stream)
         if self.events is not None:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(torch.cuda.current_stream(self.device))
@@ -238,7 +265,7 @@ class Communicator:
         parameters is captured once into a CUDA graph and then replayed (one
         launch of the whole schedule: kernels, peer flags, the allgather's
         side-stream pulls), which removes the per-call host cost."""
-        key = (mode, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), ebf, opc)
+        key = (mode, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), ebf, opc, self.ag_mode)
         if self.use_graphs and self.events is None and not torch.cuda.is_current_stream_capturing():
             g = self._graph_cache.get(key) if self._n is not None else None
             if g is not None:
@@ -330,29 +357,42 @@ class Communicator:
             sl, sz, wd = lay.slot_off[k]
             return self._addr(r, sl), self._addr(r, sz), self._addr(r, wd)
 
-        def step(inp, local, n_, acc, out_slot=None, out_blob=None):
+        def step(inp, local, n_, acc, out_slot=None, out_blob=None, post=None):
             io = _StepIO()
             if inp is not None:
                 io.in_slots, io.in_sizes, io.in_widths = inp
             if out_slot is not None:
                 io.out_slots, io.out_sizes, io.out_widths = out_slot
+                if post is not None:  # the kernel posts the peer's flag itself when done
+                    io.post_flag = self._addr(*post)
             else:
                 io.blob_out, io.blob_out_cap, io.d_len_out, io.sidecar_out = out_blob
             L.check(lib.gz_step(ctypes.byref(io), local, n_, ebf, opc, acc, tws.data_ptr(), tws.numel(),
                                 ws.status_ptr(), s), "gz_step")
 
+        own_free = None
+        if mode == "allreduce":
+            # peers must have consumed our previous own blob before the last RS
+            # step rewrites it: waited for on a side branch, off the ring's
+            # critical path (joined just before that step)
+            fork = torch.cuda.Event()
+            fork.record(cur)
+            self.copy_stream.wait_event(fork)
+            self._take_all([lay.ag_consumed(j) for j in range(N) if j != i], self.copy_stream.cuda_stream, False)
+            own_free = torch.cuda.Event()
+            own_free.record(self.copy_stream)
+
         def wait_own_blob_free():
-            # peers must have consumed our previous own blob
-            for j in range(N):
-                if j != i:
-                    self._take(lay.ag_consumed(j), s)
+            if own_free is not None:
+                cur.wait_event(own_free)
+            else:
+                self._take_all([lay.ag_consumed(j) for j in range(N) if j != i], s)
 
         def own_ready():
-            for j in range(N):
-                if j != i:
-                    self._post(j, lay.ag_ready(i), s)
+            self._post_all([(j, lay.ag_ready(i)) for j in range(N) if j != i], s)
 
         launches = 0
+        self.stamp_labels = []
         self._mark("start")
         if mode in ("allreduce", "reduce_scatter"):
             # the right neighbour must have consumed our previous writes
@@ -361,10 +401,10 @@ class Communicator:
                 if isinstance(p, Compress):
                     # step 0: compress the local chunk into our output slot 0 (slotted: no
                     # gather); the right neighbour's fused step reads it in place
-                    step(None, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot))
+                    step(None, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot),
+                         post=(p.dst, lay.rs_full(p.slot)))
                     launches += 1
                     self._mark("compress")
-                    self._post(p.dst, lay.rs_full(p.slot), s)
                 elif isinstance(p, Reduce):
                     self._take(lay.rs_full(p.slot), s)
                     inp = slot(left, p.slot)  # the left neighbour's output, read over NVLink
@@ -379,7 +419,8 @@ class Communicator:
                         continue
                     # fused decompress(recv) + op + compress
                     if not p.last:
-                        step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot + 1))
+                        step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot + 1),
+                             post=(p.dst, lay.rs_full(p.slot + 1)))
                         launches += 1
                     else:
                         wait_own_blob_free()  # our own blob is read by every peer in the allgather
@@ -388,9 +429,7 @@ class Communicator:
                                        self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1])))
                         launches += 2
                     self._mark("reduce_last" if p.last else "reduce")
-                    if not p.last:
-                        self._post(p.dst, lay.rs_full(p.slot + 1), s)
-                    else:
+                    if p.last:
                         own_ready()
         if mode == "allgather":
             # compress our chunk once into our own blob; the own chunk is kept verbatim
@@ -425,10 +464,12 @@ class Communicator:
         s = cur.cuda_stream
         ws = self.ws
         launches = 0
-        if len(owners) > 1 and self.ag_mode == "multi":
+        mode = self.ag_mode
+        if mode == "auto":
+            mode = "multi" if max(msize(chunk_of(j)) for j in owners) <= AG_MULTI_MAX else "copy"
+        if len(owners) > 1 and mode == "multi":
             # one launch decodes every owner's blob straight out of its memory
-            for j in owners:
-                self._take(lay.ag_ready(j), s)
+            self._take_all([lay.ag_ready(j) for j in owners], s)
             k = len(owners)
             P = ctypes.c_void_p * k
             blobs = P(*[self._addr(j, lay.own_off[0]) for j in owners])
@@ -437,8 +478,7 @@ class Communicator:
             ys = P(*[chunk_ptr(out, chunk_of(j)) for j in owners])
             L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s), "gz_decompress_multi")
             self._mark("decode")
-            for j in owners:
-                self._post(j, lay.ag_consumed(i), s)
+            self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
             return 1
         if len(owners) == 1:
             j = owners[0]
@@ -455,8 +495,7 @@ class Communicator:
         self.copy_stream.wait_event(rs_done)
         landed = []
         for k, j in enumerate(owners):
-            L.check(lib.gz_stream_wait_u32_geq(cs, self._addr(i, lay.ag_ready(j)), 1), "gz_stream_wait_u32_geq")
-            L.check(lib.gz_stream_write_u32(cs, self._addr(i, lay.ag_ready(j)), 0), "gz_stream_write_u32")
+            self._take_all([lay.ag_ready(j)], cs, False)
             b, sc = lay.land_off[k]
             items = (_CopyItem * 2)(
                 _CopyItem(self._addr(j, lay.own_off[0]), self._addr(i, b), self._addr(j, lay.len_off + 8 * N),
@@ -499,7 +538,12 @@ class _StepIO(ctypes.Structure):  # gz_step_io (include/gzccl.h)
     _fields_ = [("in_blob", ctypes.c_void_p), ("in_sidecar", ctypes.c_void_p), ("in_slots", ctypes.c_void_p),
                 ("in_sizes", ctypes.c_void_p), ("in_widths", ctypes.c_void_p), ("blob_out", ctypes.c_void_p),
                 ("blob_out_cap", ctypes.c_uint64), ("d_len_out", ctypes.c_void_p), ("sidecar_out", ctypes.c_void_p),
-                ("out_slots", ctypes.c_void_p), ("out_sizes", ctypes.c_void_p), ("out_widths", ctypes.c_void_p)]
+                ("out_slots", ctypes.c_void_p), ("out_sizes", ctypes.c_void_p), ("out_widths", ctypes.c_void_p),
+                ("post_flag", ctypes.c_void_p)]
+
+
+class _FlagOp(ctypes.Structure):  # gz_flag_op (include/gzccl.h)
+    _fields_ = [("ptr", ctypes.c_void_p), ("value", ctypes.c_uint32), ("kind", ctypes.c_uint32)]
 
 
 class _CopyItem(ctypes.Structure):

@@ -152,12 +152,13 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   }
   a.gshift = gs;
   a.ngctas = gbase;
-  count_launch(2);  // + the gather below
+  count_launch();
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   int rc = (int)cudaGetLastError();
   if (rc) return rc;
   if (g_dbg_flags & 1) return 0;
   if (a.slotted_out) return 0;  // slotted output: the consumer reads the slots
+  count_launch();
   // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
   static int gcap = -1;
   if (gcap < 0) {
@@ -188,6 +189,11 @@ int launch_encode(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
 }
 
 __global__ void k_record_error(Status* st, unsigned long long v) { atomicMin(&st->decode_error, v); }
+__global__ void k_stamp(unsigned long long* dst) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *dst = t;
+}
 
 __global__ void k_copy_blob(const uint4* __restrict__ src, uint4* __restrict__ dst, const uint64_t* d_len, uint64_t max_bytes) {
   const uint64_t len = umin64(*d_len, max_bytes);
@@ -239,6 +245,7 @@ struct IpcHandle {
 typedef CUresult (*PFN_addrRange)(CUdeviceptr*, size_t*, CUdeviceptr);
 typedef CUresult (*PFN_writeValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
 typedef CUresult (*PFN_waitValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+typedef CUresult (*PFN_batchMemOp)(CUstream, unsigned int, CUstreamBatchMemOpParams*, unsigned int);
 
 template <typename F>
 F driver_fn(const char* name) {
@@ -258,6 +265,10 @@ PFN_writeValue32 p_write32() {
 }
 PFN_waitValue32 p_wait32() {
   static PFN_waitValue32 f = driver_fn<PFN_waitValue32>("cuStreamWaitValue32");
+  return f;
+}
+PFN_batchMemOp p_batch() {
+  static PFN_batchMemOp f = driver_fn<PFN_batchMemOp>("cuStreamBatchMemOp");
   return f;
 }
 
@@ -308,6 +319,11 @@ extern "C" {
 int gz_debug_set_timestamps(void* p) {
   g_dbg = reinterpret_cast<unsigned long long*>(p);
   return 0;
+}
+// profiling only: write the GPU's %globaltimer (ns) into *dst, stream-ordered
+int gz_debug_stamp(void* dst, gz_stream_t stream) {
+  k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(dst));
+  return (int)cudaGetLastError();
 }
 // experiments only: bit 0 = skip the gather kernel (output incomplete)
 int gz_debug_set_flags(int f) {
@@ -529,10 +545,10 @@ int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int
     a.seg[0] = Seg{local, m, nullptr, nullptr, nullptr, io->out_widths, 0, 0, 0, 0};
     a.tile_rel = io->out_sizes;
     a.scratch = io->out_slots;
-    a.slotted_out = 1;
-    // the gather that would reset the tile-claim counter is skipped
-    cudaMemsetAsync(&wv.hdr->claim, 0, sizeof(unsigned int), (cudaStream_t)stream);
+    a.slotted_out = 1;  // the encoder's last CTA re-zeroes the claim counter (no gather)
+    a.post_flag = reinterpret_cast<unsigned int*>(io->post_flag);
   } else {
+    if (io->post_flag) return GZ_EINVAL;
     SidecarView so = sidecar_view(io->sidecar_out, m);
     a.seg[0] = Seg{local, m, io->blob_out, io->d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
   }
@@ -541,10 +557,7 @@ int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int
   a.st = reinterpret_cast<Status*>(d_status);
   a.op = op;
   a.acc_out = acc_out;
-  auto done = [&](int rc) {  // a slotted launch leaves the claim counter at 0 for the next user
-    if (!rc && slotted) rc = (int)cudaMemsetAsync(&wv.hdr->claim, 0, sizeof(unsigned int), (cudaStream_t)stream);
-    return rc;
-  };
+  auto done = [](int rc) { return rc; };
   if (!fused) return done(launch_encode<SRC_PLAIN, 1>(a, ntiles_of(m), (cudaStream_t)stream));
   a.in_tw = 2.0 * eb;
   if (io->in_slots) {
@@ -682,6 +695,29 @@ int gz_stream_write_u32(gz_stream_t stream, void* dptr, uint32_t value) {
 int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value) {
   if (!p_wait32()) return (int)cudaErrorNotSupported;
   CUresult r = p_wait32()((CUstream)stream, (CUdeviceptr)dptr, value, CU_STREAM_WAIT_VALUE_GEQ);
+  return r == CUDA_SUCCESS ? 0 : (int)r + 20000;
+}
+
+int gz_stream_flag_ops(gz_stream_t stream, const gz_flag_op* ops, uint32_t count) {
+  if (!ops || count == 0 || count > GZ_MAX_FLAG_OPS) return GZ_EINVAL;
+  if (!p_batch()) return (int)cudaErrorNotSupported;
+  CUstreamBatchMemOpParams p[GZ_MAX_FLAG_OPS];
+  std::memset(p, 0, sizeof(p));
+  for (uint32_t i = 0; i < count; ++i) {
+    if (!ops[i].ptr || ops[i].kind > 1) return GZ_EINVAL;
+    if (ops[i].kind == 0) {
+      p[i].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
+      p[i].writeValue.address = (CUdeviceptr)ops[i].ptr;
+      p[i].writeValue.value = ops[i].value;
+      p[i].writeValue.flags = CU_STREAM_WRITE_VALUE_DEFAULT;
+    } else {
+      p[i].waitValue.operation = CU_STREAM_MEM_OP_WAIT_VALUE_32;
+      p[i].waitValue.address = (CUdeviceptr)ops[i].ptr;
+      p[i].waitValue.value = ops[i].value;
+      p[i].waitValue.flags = CU_STREAM_WAIT_VALUE_GEQ;
+    }
+  }
+  CUresult r = p_batch()((CUstream)stream, count, p, 0);
   return r == CUDA_SUCCESS ? 0 : (int)r + 20000;
 }
 

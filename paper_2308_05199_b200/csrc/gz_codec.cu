@@ -56,6 +56,7 @@ struct EncodeArgs {
   int op;
   float* acc_out;          // optional: reduced values (f32)
   int slotted_out;         // 1: the output stays in slotted form (scratch/tile_rel), no gather
+  unsigned int* post_flag; // slotted only, may be null: set to 1 once the whole output is written
 };
 
 
@@ -642,6 +643,24 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
+  if (a.slotted_out) {
+    // no gather kernel follows: the last CTA re-zeroes the claim counter and
+    // posts the step's completion flag (a peer's, over NVLink) itself, so a
+    // ring step is one wait node + this kernel
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      if (atomicAdd(&a.ws->done, 1ull) == gridDim.x - 1) {
+        a.ws->claim = 0;
+        a.ws->done = 0;
+        if (a.post_flag) {
+          __threadfence_system();
+          asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(a.post_flag), "r"(1u) : "memory");
+        }
+      }
+    }
+  }
   if (a.dbg && lane == 0) {  // experiments: per-warp timestamps
     unsigned long long* d = a.dbg + (c * NW + warp) * 12;
     unsigned smid;

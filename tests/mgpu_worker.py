@@ -50,27 +50,36 @@ def main():
                 for r in range(world)]
         expect = O.ring_allreduce(bufs, eb, op)
         x = torch.from_numpy(bufs[rank]).to(dev)
-        out = c.ring_allreduce(x, eb, op)
-        torch.cuda.synchronize()
-        if out.cpu().numpy().tobytes() != expect[rank].tobytes():
-            failures.append(f"oracle n={n} op={op} eb={eb}")
-        checked += 1
+        for mode in ("copy", "multi", "auto"):  # the allgather's two data paths
+            c.ag_mode = mode
+            out = c.ring_allreduce(x, eb, op)
+            torch.cuda.synchronize()
+            if out.cpu().numpy().tobytes() != expect[rank].tobytes():
+                failures.append(f"oracle n={n} op={op} eb={eb} ag_mode={mode}")
+            checked += 1
+    c.ag_mode = "auto"
     # repeated calls on the same tensors are replayed from a captured CUDA graph
     n = 3_000_017
     bufs = [O.smooth_field(n, 0.21 * r) + np.random.default_rng(900 + r).normal(0, 1e-3, n).astype(np.float32)
             for r in range(world)]
     expect = O.ring_allreduce(bufs, 1e-4, "sum")[rank].tobytes()
-    x = torch.from_numpy(bufs[rank]).to(dev)
-    out = torch.empty_like(x)
-    for rep in range(5):
-        if rep == 3:
-            x.copy_(torch.from_numpy(bufs[(rank + 1) % world]))  # new values, same tensors: the graph sees them
-            expect = O.ring_allreduce([bufs[(r + 1) % world] for r in range(world)], 1e-4, "sum")[rank].tobytes()
-        c.ring_allreduce(x, 1e-4, "sum", out=out)
-        torch.cuda.synchronize()
-        if out.cpu().numpy().tobytes() != expect:
-            failures.append(f"graph replay rep={rep}")
-        checked += 1
+    expect0 = expect
+    expect1 = O.ring_allreduce([bufs[(r + 1) % world] for r in range(world)], 1e-4, "sum")[rank].tobytes()
+    for mode in ("copy", "multi"):
+        c.ag_mode = mode
+        x = torch.from_numpy(bufs[rank]).to(dev)
+        out = torch.empty_like(x)
+        expect = expect0
+        for rep in range(5):
+            if rep == 3:
+                x.copy_(torch.from_numpy(bufs[(rank + 1) % world]))  # new values, same tensors: the graph sees them
+                expect = expect1
+            c.ring_allreduce(x, 1e-4, "sum", out=out)
+            torch.cuda.synchronize()
+            if out.cpu().numpy().tobytes() != expect:
+                failures.append(f"graph replay rep={rep} ag_mode={mode}")
+            checked += 1
+    c.ag_mode = "auto"
     if not c._graph_cache:
         failures.append("no graph was captured")
     # standalone reduce-scatter and allgather(v) (collectives.py:247-291), vs the oracle,
