@@ -122,7 +122,10 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_encode<SRC, NSEG, FAST>, 32 * NW, smem);
     cap = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
   }
-  uint64_t G = std::min<uint64_t>((uint64_t)cap, std::max<uint64_t>(1, (total_tiles + NW - 1) / NW));
+  // one CTA per tile up to one per SM: a small message is spread over as many
+  // SMs as it has tiles (a tile's encode is a latency chain of ~1100
+  // instructions; 24 tiles on one SM would serialise on its issue slots)
+  uint64_t G = std::min<uint64_t>((uint64_t)cap, std::max<uint64_t>(1, total_tiles));
   G = std::max<uint64_t>(G, (uint64_t)a.nseg);
   if (G > (uint64_t)MAXGRID) return GZ_EINVAL;
   uint64_t base = 0, left = G - (uint64_t)a.nseg;
@@ -135,13 +138,15 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   a.nctas = base;
   a.total_tiles = total_tiles;
   // tiles per gather group (one warp each): 8, doubled until the groups fit
-  // MAXGRID
+  // MAXGRID; halved (down to 1) while there are fewer groups than ~8 warps
+  // per SM -- a small message's gather is a per-warp latency chain
   uint32_t gs = 3;
   auto ngroups = [&](uint32_t sh) {
     uint64_t g = 0;
     for (int k = 0; k < a.nseg; ++k) g += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << sh) - 1) >> sh);
     return g;
   };
+  while (gs > 0 && ngroups(gs) < 1184) --gs;
   while (ngroups(gs) > (uint64_t)MAXGRID && gs < 10) ++gs;
   if (ngroups(gs) > (uint64_t)MAXGRID) return GZ_EINVAL;
   uint64_t gbase = 0;

@@ -36,7 +36,7 @@ struct EncodeArgs {
   int nseg;
   uint64_t nctas;          // encoder CTAs (== grid), split over segments by cta_base
   uint64_t ngctas;         // gather groups (one warp each), 2^gshift tiles each, split by gcta_base
-  uint32_t gshift;         // log2(tiles per gather group), 3..10
+  uint32_t gshift;         // log2(tiles per gather group), 0..10
   uint64_t total_tiles;    // tiles over all segments
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)

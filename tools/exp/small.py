@@ -4,6 +4,8 @@ import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2308_05199_b200._lib as L
+if os.environ.get("GZ_LIB"):
+    L.LIB_PATH = os.environ["GZ_LIB"]
 import paper_2308_05199_b200 as gz
 from oracle import oracle as O
 
