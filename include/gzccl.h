@@ -130,6 +130,9 @@ typedef struct {
   uint8_t* out_widths;
   uint32_t* post_flag; /* slotted output only, may be NULL: the kernel stores 1 here (e.g. a peer's flag,
                           IPC-mapped) once the whole output is written -- a fused gz_stream_write_u32 */
+  uint32_t* wait_flag; /* slotted output only, may be NULL: the kernel waits until this (own-memory) flag
+                          is >= 1 before reading its inputs and resets it to 0 when done -- a fused
+                          wait + reset (bounded: traps after ~20 s) */
 } gz_step_io;
 uint64_t gz_slots_bytes(uint64_t m);
 int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,

@@ -552,8 +552,9 @@ int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int
     a.scratch = io->out_slots;
     a.slotted_out = 1;  // the encoder's last CTA re-zeroes the claim counter (no gather)
     a.post_flag = reinterpret_cast<unsigned int*>(io->post_flag);
+    a.wait_flag = reinterpret_cast<unsigned int*>(io->wait_flag);
   } else {
-    if (io->post_flag) return GZ_EINVAL;
+    if (io->post_flag || io->wait_flag) return GZ_EINVAL;
     SidecarView so = sidecar_view(io->sidecar_out, m);
     a.seg[0] = Seg{local, m, io->blob_out, io->d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
   }

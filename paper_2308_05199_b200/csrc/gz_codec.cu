@@ -57,7 +57,9 @@ struct EncodeArgs {
   float* acc_out;          // optional: reduced values (f32)
   int slotted_out;         // 1: the output stays in slotted form (scratch/tile_rel), no gather
   unsigned int* post_flag; // slotted only, may be null: set to 1 once the whole output is written
+  unsigned int* wait_flag; // slotted only, may be null: wait until >= 1 before reading inputs, reset to 0
 };
+
 
 
 // Fused step: the local values are loaded for the current tile only and the
@@ -99,6 +101,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
+}
+
+// Wait (thread 0) until *flag >= 1, written by a peer GPU; a release/acquire
+// pair with the producer's __threadfence_system + store.  Bounded: a flag
+// that never arrives traps after ~20 s instead of hanging the GPU.
+__device__ __forceinline__ void wait_flag_sys(const unsigned int* flag) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+  if (v >= 1u) return;
+  const unsigned long long t0 = gtimer();
+  do {
+    __nanosleep(64);
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
+    if (gtimer() - t0 > 20000000000ull) __trap();
+  } while (v < 1u);
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -545,7 +562,10 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   float* xsb1 = ONEBUF ? xsb0 : reinterpret_cast<float*>(my + TILE_VALUES * 4);
   uint32_t* stg0 = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4);  // fused step only
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
-  if (tid == 0) s_next = 0;
+  if (tid == 0) {
+    s_next = 0;
+    if (a.wait_flag) wait_flag_sys(a.wait_flag);  // the ring's "input ready" (or "slots free") flag
+  }
   __syncthreads();
   const uint64_t c = blockIdx.x;
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
@@ -654,6 +674,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
       if (atomicAdd(&a.ws->done, 1ull) == gridDim.x - 1) {
         a.ws->claim = 0;
         a.ws->done = 0;
+        if (a.wait_flag) *reinterpret_cast<volatile unsigned int*>(a.wait_flag) = 0u;  // every CTA has passed it
         if (a.post_flag) {
           __threadfence_system();
           asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(a.post_flag), "r"(1u) : "memory");

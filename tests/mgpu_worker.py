@@ -52,12 +52,14 @@ def main():
         x = torch.from_numpy(bufs[rank]).to(dev)
         for mode in ("copy", "multi", "auto"):  # the allgather's two data paths
             c.ag_mode = mode
+            c.kernel_waits = mode != "copy"  # ring flags taken by stream wait nodes or inside the kernels
             out = c.ring_allreduce(x, eb, op)
             torch.cuda.synchronize()
             if out.cpu().numpy().tobytes() != expect[rank].tobytes():
                 failures.append(f"oracle n={n} op={op} eb={eb} ag_mode={mode}")
             checked += 1
     c.ag_mode = "auto"
+    c.kernel_waits = True
     # repeated calls on the same tensors are replayed from a captured CUDA graph
     n = 3_000_017
     bufs = [O.smooth_field(n, 0.21 * r) + np.random.default_rng(900 + r).normal(0, 1e-3, n).astype(np.float32)
