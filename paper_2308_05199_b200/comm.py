@@ -128,11 +128,13 @@ class Communicator:
         self._last_key = None
         # allgather: "multi" (one launch decodes every owner's blob out of its memory), "copy" (pull each
         # blob over NVLink on a side stream, decode it locally) or "auto" (multi for chunks up to
-        # AG_MULTI_MAX values, where it wins by up to ~30 µs per call at N = 4; copy above)
+        # AG_MULTI_MAX values, where it wins by up to ~30 µs per call at N = 4; copy above -- also at
+        # N = 2, where it beats decoding the single owner's blob out of peer memory by ~2.5 % at 512 MiB)
         self.ag_mode = "auto"
         # intermediate reduce-scatter steps take their input flag inside the kernel (one CTA
         # thread polls, bounded) instead of a stream wait node: ~5 µs less per step
         self.kernel_waits = True
+        self.early_pull = False  # allreduce: allgather pulls start when each owner is ready, not after our last step
 
     # ------------------------------------------------------------------ setup
     def _setup(self, m_max: int):
@@ -268,7 +270,7 @@ class Communicator:
         parameters is captured once into a CUDA graph and then replayed (one
         launch of the whole schedule: kernels, peer flags, the allgather's
         side-stream pulls), which removes the per-call host cost."""
-        key = (mode, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), ebf, opc, self.ag_mode, self.kernel_waits)
+        key = (mode, x.data_ptr(), x.numel(), out.data_ptr(), out.numel(), ebf, opc, self.ag_mode, self.kernel_waits, self.early_pull)
         if self.use_graphs and self.events is None and not torch.cuda.is_current_stream_capturing():
             g = self._graph_cache.get(key) if self._n is not None else None
             if g is not None:
@@ -456,13 +458,14 @@ class Communicator:
             # compress-once allgather; owner j's chunk is chunk_of(j)
             owners = [(i - 1 - k) % N for k in range(N - 1)]  # the order the ring delivers them
             chunk_of = (lambda j: (j + 1) % N) if mode == "allreduce" else (lambda j: j)
-            launches += self._allgather_pull(owners, chunk_of, chunk_ptr, msize, out, ebf, cur)
+            launches += self._allgather_pull(owners, chunk_of, chunk_ptr, msize, out, ebf, cur,
+                                             forked=own_free is not None)
         # our slots are free again: the left neighbour may write the next call's steps
         self._post(left, lay.rs_consumed(), s)
         self.epoch = e
         self.launches_per_call = launches
 
-    def _allgather_pull(self, owners, chunk_of, chunk_ptr, msize, out, ebf, cur) -> int:
+    def _allgather_pull(self, owners, chunk_of, chunk_ptr, msize, out, ebf, cur, forked=False) -> int:
         """A side stream pulls each owner's blob + sidecar over NVLink into our
         (free) reduce-scatter slots with one bulk copy and releases the owner;
         the main stream decodes it from local HBM as soon as it has landed,
@@ -490,7 +493,7 @@ class Communicator:
             self._mark("decode")
             self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
             return 1
-        if len(owners) == 1:
+        if len(owners) == 1 and mode != "copy":  # N = 2, small chunk: decode straight from the peer
             j = owners[0]
             c = chunk_of(j)
             self._take(lay.ag_ready(j), s)
@@ -500,9 +503,13 @@ class Communicator:
             self._post(j, lay.ag_consumed(i), s)
             return 1
         cs = self.copy_stream.cuda_stream
-        rs_done = torch.cuda.Event()
-        rs_done.record(cur)
-        self.copy_stream.wait_event(rs_done)
+        if not forked or not self.early_pull:
+            # the landing slots are free once the previous call's decodes are done:
+            # the allreduce's side stream is already ordered after them (forked at
+            # the call's start), so its pulls start as soon as each owner is ready
+            rs_done = torch.cuda.Event()
+            rs_done.record(cur)
+            self.copy_stream.wait_event(rs_done)
         landed = []
         for k, j in enumerate(owners):
             self._take_all([lay.ag_ready(j)], cs, False)

@@ -1,0 +1,10 @@
+# refresh: all gpu tests (4 GPUs), smoke, bench N=1/2/4, cfg4 sweep at N=4
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -1
+timeout 600 python bench.py --steps 20 --warmup 3 > gpurun_out/r2_bench_n1.json 2>gpurun_out/r2_bench_n1.err; echo "n1 rc=$?"; cat gpurun_out/r2_bench_n1.json
+for N in 2 4; do
+timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2952$N bench.py --gpus $N --steps 10 --warmup 3 > gpurun_out/r2_bench_n$N.json 2>gpurun_out/r2_bench_n$N.err; echo "n$N rc=$?"; tail -1 gpurun_out/r2_bench_n$N.json
+done
+timeout 1200 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29530 tools/sweep_allreduce.py 1024 > gpurun_out/r2_sweep_n4.md 2>gpurun_out/r2_sweep_n4.err; echo "sweep rc=$?"; cat gpurun_out/r2_sweep_n4.md

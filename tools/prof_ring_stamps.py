@@ -24,6 +24,8 @@ def main():
         c.stamps = torch.zeros(128, dtype=torch.int64, device=dev)
         if os.environ.get("GZ_AG_MODE"):
             c.ag_mode = os.environ["GZ_AG_MODE"]
+        if os.environ.get("GZ_EARLY_PULL"):
+            c.early_pull = os.environ["GZ_EARLY_PULL"] == "1"
         if os.environ.get("GZ_NO_STAMPS"):
             c.stamps = None
         out = torch.empty_like(x)
