@@ -237,12 +237,13 @@ class Communicator:
         """post flags in several peers' memory: [(rank, off)] (one batch)"""
         self._flag_ops([(0, self._addr(r, off), 1) for r, off in targets], s)
 
-    def _mark(self, label: str):
+    def _mark(self, label: str, stream: int | None = None):
         if self.stamps is not None:  # profiling: device timestamps, also inside a captured graph
             k = len(self.stamp_labels)
             if k < self.stamps.numel():
                 self.stamp_labels.append(label)
-                L.lib().gz_debug_stamp(self.stamps.data_ptr() + 8 * k, torch.cuda.current_stream(self.device).cuda_stream)
+                s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+                L.lib().gz_debug_stamp(self.stamps.data_ptr() + 8 * k, s)
         if self.events is not None:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(torch.cuda.current_stream(self.device))
@@ -493,6 +494,30 @@ class Communicator:
             self._mark("decode")
             self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
             return 1
+        if mode == "bulk":
+            # pull every owner's blob + sidecar in ONE copy launch (the NVLink ingress is the
+            # bound; a decode beside a pull runs barely faster than after it), then decode
+            # them all from local HBM in one launch
+            self._take_all([lay.ag_ready(j) for j in owners], s)
+            items = []
+            for k, j in enumerate(owners):
+                b, sc = lay.land_off[k]
+                items.append(_CopyItem(self._addr(j, lay.own_off[0]), self._addr(i, b), self._addr(j, lay.len_off + 8 * N),
+                                       lay.blob_cap))
+                items.append(_CopyItem(self._addr(j, lay.own_off[1]), self._addr(i, sc), None,
+                                       int(lib.gz_sidecar_bytes(msize(chunk_of(j))))))
+            L.check(lib.gz_copy_items_sms((_CopyItem * len(items))(*items), len(items), 0, s), "gz_copy_items_sms")
+            self._mark("copy")
+            self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
+            k = len(owners)
+            P = ctypes.c_void_p * k
+            blobs = P(*[self._addr(i, lay.land_off[q][0]) for q in range(k)])
+            scs = P(*[self._addr(i, lay.land_off[q][1]) for q in range(k)])
+            ns = (ctypes.c_uint64 * k)(*[msize(chunk_of(j)) for j in owners])
+            ys = P(*[chunk_ptr(out, chunk_of(j)) for j in owners])
+            L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s), "gz_decompress_multi")
+            self._mark("decode")
+            return 2
         if len(owners) == 1 and mode != "copy":  # N = 2, small chunk: decode straight from the peer
             j = owners[0]
             c = chunk_of(j)
@@ -522,6 +547,7 @@ class Communicator:
             # the first pull has the GPU to itself; later ones run beside a decode
             L.check(lib.gz_copy_items_sms(items, 2, AG_COPY_SMS if k else 0, cs), "gz_copy_items_sms")
             launches += 1
+            self._mark("copy", cs)
             self._post(j, lay.ag_consumed(i), cs)
             ev = torch.cuda.Event()
             ev.record(self.copy_stream)

@@ -706,11 +706,12 @@ int gz_stream_wait_u32_geq(gz_stream_t stream, void* dptr, uint32_t value) {
 
 int gz_stream_flag_ops(gz_stream_t stream, const gz_flag_op* ops, uint32_t count) {
   if (!ops || count == 0 || count > GZ_MAX_FLAG_OPS) return GZ_EINVAL;
+  for (uint32_t i = 0; i < count; ++i)
+    if (!ops[i].ptr || ops[i].kind > 1) return GZ_EINVAL;
   if (!p_batch()) return (int)cudaErrorNotSupported;
   CUstreamBatchMemOpParams p[GZ_MAX_FLAG_OPS];
   std::memset(p, 0, sizeof(p));
   for (uint32_t i = 0; i < count; ++i) {
-    if (!ops[i].ptr || ops[i].kind > 1) return GZ_EINVAL;
     if (ops[i].kind == 0) {
       p[i].writeValue.operation = CU_STREAM_MEM_OP_WRITE_VALUE_32;
       p[i].writeValue.address = (CUdeviceptr)ops[i].ptr;

@@ -48,6 +48,15 @@ def test_host_sizing_functions():
     assert L.gz_compress(None, 10, 1e-4, 64, None, 0, None, None, None, None, 0, None, None) == _lib.GZ_EBLOCK
     assert L.gz_compress(None, 10, -1.0, 32, None, 0, None, None, None, None, 0, None, None) == _lib.GZ_EBOUND
     assert L.gz_compress(None, 10, 1e-4, 32, None, 0, None, None, None, None, 0, None, None) == _lib.GZ_EINVAL
+    # flag batches: empty, oversized and null-pointer batches are refused before any driver call
+    from paper_2308_05199_b200.comm import _FlagOp
+
+    ops = (_FlagOp * 65)()
+    assert L.gz_stream_flag_ops(None, ops, 0) == _lib.GZ_EINVAL
+    assert L.gz_stream_flag_ops(None, ops, 65) == _lib.GZ_EINVAL
+    assert L.gz_stream_flag_ops(None, ops, 1) == _lib.GZ_EINVAL  # ptr NULL
+    bad = (_FlagOp * 1)(_FlagOp(0x1000, 1, 7))  # unknown kind
+    assert L.gz_stream_flag_ops(None, bad, 1) == _lib.GZ_EINVAL
 
 
 def test_chunk_spans_and_tree_match_reference_semantics(oracle):

@@ -2,6 +2,7 @@
 cd $GRAFT_REPO_ROOT
 for N in 4 2; do
 T="timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 2951$N tools/prof_ring_stamps.py"
-for ep in 0 1; do for m in auto copy; do
-  echo "== N=$N early_pull=$ep ag_mode=$m"; GZ_EARLY_PULL=$ep GZ_AG_MODE=$m GZ_NO_STAMPS=1 $T 64 512 2>&1 | grep "rank0"
-done; done; done
+for m in auto bulk multi; do
+  echo "== N=$N ag_mode=$m"; GZ_AG_MODE=$m GZ_NO_STAMPS=1 $T 16 64 512 2>&1 | grep "rank0"
+done; done
+GZ_AG_MODE=bulk timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29519 tools/prof_ring_stamps.py 512 2>&1 | grep "MiB rank0"
