@@ -76,3 +76,22 @@ def both(r, budget):
 for r, b in ((24, 24), (48, 48), (0, 24), (24, 8), (12, 12)):
     print(f"decode reserve {r} + copy budget {b} concurrently: {timeit(lambda: both(r, b)):.1f} us")
 print(f"copy alone budget 24: {timeit(lambda: (copy(24), cur.wait_stream(cs))):.1f} us")
+
+
+def ce(n_bytes=LB):
+    with torch.cuda.stream(cs):
+        land[:n_bytes].copy_(peer[:n_bytes], non_blocking=True)
+
+
+def both_ce(r):
+    ev = torch.cuda.Event()
+    ev.record(cur)
+    cs.wait_event(ev)
+    ce()
+    dec(r)
+    cur.wait_stream(cs)
+
+
+print(f"CE copy alone: {timeit(lambda: (ce(), cur.wait_stream(cs))):.1f} us")
+for r in (0, 8):
+    print(f"decode reserve {r} + CE copy concurrently: {timeit(lambda: both_ce(r)):.1f} us")
