@@ -191,7 +191,15 @@ def bench_codec(args):
     tws = ws.tile_ws(int(lib.gz_workspace_bytes(n)))
     y = torch.empty(n, dtype=torch.float32, device=dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    flush_r = torch.ones(256 << 20, dtype=torch.uint8, device=dev).view(torch.int64)
     stream = torch.cuda.current_stream()
+
+    def l2_flush():
+        # 256 MB write (> 126 MB L2), then a 256 MB read: the read evicts the
+        # write's dirty lines, so their write-back does not land inside the
+        # timed region and L2 holds none of the step's data
+        flush.zero_()
+        flush_r.sum()
     s = stream.cuda_stream
 
     def comp():
@@ -203,7 +211,7 @@ def bench_codec(args):
                 "gz_decompress_sidecar")
 
     for _ in range(max(args.warmup, 3)):
-        flush.zero_()
+        l2_flush()
         comp()
         dec()
     torch.cuda.synchronize()
@@ -212,7 +220,7 @@ def bench_codec(args):
     with ClockSampler(0) as clk:
         torch.cuda.synchronize()
         for _ in range(args.steps):
-            flush.zero_()  # L2 flush: 256 MB > 126 MB L2, outside the timed events
+            l2_flush()  # outside the timed events
             e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
             e0.record(stream)
             comp()
@@ -232,6 +240,55 @@ def bench_codec(args):
     value = (bytes_c + bytes_d) / (t_c + t_d) / 1e9
     peak, peak_kind = peaks()
     achieved_c = bytes_c / t_c / 1e9
+
+    # supplementary: the compressor on a field larger than L2 (2^27 values,
+    # 512 MB; same synthetic field, no flush needed), where the per-call fixed
+    # cost no longer dominates -- reported in config, not as the line's value
+    big = {}
+    try:
+        nb = 1 << 27
+        xb = torch.from_numpy(O.smooth_field(nb)).to(dev)
+        capb = int(lib.gz_compress_bound(nb))
+        outb = torch.empty(capb, dtype=torch.uint8, device=dev)
+        scb = torch.empty(int(lib.gz_sidecar_bytes(nb)), dtype=torch.uint8, device=dev)
+        twb = gz.Workspace(dev)
+        twb.reset_status()
+        twsb = twb.tile_ws(int(lib.gz_workspace_bytes(nb)))
+        yb_ = torch.empty(nb, dtype=torch.float32, device=dev)
+
+        def comp_b():
+            L.check(lib.gz_compress(xb.data_ptr(), nb, EB, 32, outb.data_ptr(), capb, twb.len_ptr(), scb.data_ptr(),
+                                    None, twsb.data_ptr(), twsb.numel(), twb.status_ptr(), s), "gz_compress")
+
+        def dec_b():
+            L.check(lib.gz_decompress_sidecar(outb.data_ptr(), scb.data_ptr(), nb, EB, yb_.data_ptr(),
+                                              twb.status_ptr(), s), "gz_decompress_sidecar")
+        for _ in range(3):
+            comp_b()
+            dec_b()
+        torch.cuda.synchronize()
+        Lbb = int(twb.status[4].item())
+        tcb, tdb = [], []
+        for _ in range(max(5, min(args.steps, 20))):
+            e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+            e0.record(stream)
+            comp_b()
+            e1.record(stream)
+            dec_b()
+            e2.record(stream)
+            torch.cuda.synchronize()
+            tcb.append(e0.elapsed_time(e1) * 1e-3)
+            tdb.append(e1.elapsed_time(e2) * 1e-3)
+        tcb_m, tdb_m = sorted(tcb)[len(tcb) // 2], sorted(tdb)[len(tdb) // 2]
+        big = {"values": nb, "compressed_bytes": Lbb, "compress_us": round(tcb_m * 1e6, 1),
+               "decompress_us": round(tdb_m * 1e6, 1),
+               "compress_hbm_gbs": round((4 * nb + Lbb) / tcb_m / 1e9, 1),
+               "compress_frac": round((4 * nb + Lbb) / tcb_m / 1e9 / peak, 4),
+               "decompress_hbm_gbs": round((4 * nb + Lbb) / tdb_m / 1e9, 1),
+               "decompress_frac": round((4 * nb + Lbb) / tdb_m / 1e9 / peak, 4), "stat": "median"}
+        del xb, outb, scb, twsb, yb_
+    except Exception as e:  # a supplementary number must not sink the line
+        big = {"error": str(e)[:200]}
 
     # e2e through the public API with host buffers: inputs in pinned host
     # memory; each step = H2D + compress + D2H of the blob, then H2D of the
@@ -268,9 +325,10 @@ def bench_codec(args):
         "data": "synthetic smooth field 0.5 sin(2pi i/65536) + 0.25 sin(2pi i/4099)",
         "config": {"workload": "cfg1 compress/decompress round trip, 2^24 f32, eb=1e-4, block=32",
                    "compressed_bytes": Lb, "compression_ratio": round(4 * n / Lb, 4),
-                   "l2": "flushed (256 MB write) before every timed step",
+                   "l2": "flushed before every timed step (256 MB write, then 256 MB read so no dirty line is written back inside the timed region)",
                    "compress_us": round(t_c * 1e6, 2), "decompress_us": round(t_d * 1e6, 2),
-                   "compress_hbm_gbs": round(achieved_c, 1), "decompress_hbm_gbs": round(bytes_d / t_d / 1e9, 1)},
+                   "compress_hbm_gbs": round(achieved_c, 1), "decompress_hbm_gbs": round(bytes_d / t_d / 1e9, 1),
+                   "codec_2p27": big},
         "roofline": {"bound": "hbm", "kernel": "compress = k_tile_encode + k_gather", "achieved": round(achieved_c, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved_c / peak, 4),
                      "traffic": traffic, "algorithmic_bytes_per_launch": bytes_c},
