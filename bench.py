@@ -514,6 +514,13 @@ def bench_allreduce(args):
 
     value = S_CFG2 / t / 1e9
     peak, peak_kind = peaks()
+    step_traffic = None  # ncu DRAM bytes of the fused step, measured for the 2^25-value chunk (N = 4)
+    if m == 1 << 25:
+        try:
+            with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+                step_traffic = json.load(f).get("fused_step_2p25")
+        except Exception:
+            step_traffic = None
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
@@ -530,7 +537,7 @@ def bench_allreduce(args):
                        "l2": "inputs (512 MiB) larger than L2"},
             "roofline": {"bound": "hbm", "kernel": "fused RS step = k_tile_encode<STEP> + k_gather",
                          "achieved": round(step_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                         "frac": round(step_gbs / peak, 4), "traffic": None,
+                         "frac": round(step_gbs / peak, 4), "traffic": step_traffic,
                          "algorithmic_bytes_per_launch": int(step_bytes), "avg_step_us": round(t_step * 1e6, 2)},
             "e2e": {"value": round(S_CFG2 / t_e2e / 1e9, 3), "unit": "GB/s", "h2d_bytes_per_step": 4 * n,
                     "d2h_bytes_per_step": 4 * n,
