@@ -98,7 +98,7 @@ def _worker(rank, world, port, case_idx, q):
     dist.destroy_process_group()
 
 
-CASES = [(k, c) for k, c in enumerate(G.ring_cases()) if c.algo == "ring-allreduce" and 2 <= c.N <= 4]
+CASES = [(k, c) for k, c in enumerate(G.ring_cases()) if c.algo == "ring-allreduce" and 2 <= c.N <= 8]
 
 
 @pytest.mark.parametrize("k,case", CASES, ids=[f"N{c.N}-n{c.n}-{c.op}" for _, c in CASES])
