@@ -42,7 +42,7 @@ struct EncodeArgs {
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
   TileWs* ws;
   unsigned long long* dbg; // optional per-warp timestamps (experiments)
-  int dbg_flags;           // experiments: bit 1 = gather kernel skips its work
+  int dbg_flags;           // experiments: bit 1 = gather kernel skips its work, bits 4-6 = global claim share
   uint32_t* tile_rel;      // per tile: compressed size (phase A -> phase B)
   uint8_t* scratch;        // per tile one TILE_SLOT-byte slot (16-byte aligned)
   Status* st;
@@ -571,14 +571,17 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
   const unsigned long long ts0 = a.dbg ? gtimer() : 0;
 
-  // ---- tile claiming (over all segments): 7/8 of the tiles are split into
+  // ---- tile claiming (over all segments): most tiles are split into
   // contiguous per-CTA ranges claimed through a shared-memory counter (warps
-  // of one SM do not get equal issue slots); the last 1/8 is claimed from one
-  // global counter, so SMs that run faster take more of the tail.  The next
+  // of one SM do not get equal issue slots); the last 1/2^tshift is claimed
+  // from one global counter, so SMs that run faster take more of the tail.  The next
   // claim is always one tile ahead (prefetch).
   const unsigned int total = (unsigned int)a.total_tiles;
-  // (the fused step's tiles take twice as long: it claims every tile globally)
-  const unsigned int stat = total - (total >> 3);
+  // global share 1/2^tshift: 1/32 for plain compression (2^24: 52 -> 48 us
+  // vs 1/8, tools/exp/tail.py; no change at 2^27), 1/8 for the fused step
+  const unsigned tdef = SRC == SRC_PLAIN ? 5u : 3u;
+  const unsigned tshift = ((a.dbg_flags >> 4) & 7) ? ((a.dbg_flags >> 4) & 7) : tdef;  // experiments: bits 4-6
+  const unsigned int stat = total - (total >> tshift);
   const unsigned int r0 = (unsigned int)(((uint64_t)stat * c) / gridDim.x);
   const unsigned int nr = (unsigned int)(((uint64_t)stat * (c + 1)) / gridDim.x) - r0;
   const unsigned s_next_addr = (unsigned)__cvta_generic_to_shared(&s_next);
