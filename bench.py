@@ -353,7 +353,7 @@ def _max_over_ranks(v: float, dev) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([v], device=dev, dtype=torch.float64)
+    t = torch.tensor([v], device="cpu" if dist.get_backend() == "gloo" else dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -369,9 +369,17 @@ def bench_allreduce(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    # more ranks than GPUs (tools/gpu_n8_rehearsal.sh): ranks share GPUs, NCCL (one rank
+    # per GPU) is replaced by gloo for the object plumbing and the NCCL comparators are
+    # skipped; the numbers of such a run are a code-path rehearsal, not a measurement
+    oversub = world > torch.cuda.device_count()
+    local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     lib = L.lib()
     n = S_CFG2 // 4
     xh = O.smooth_field(n, 0.37 * rank)
@@ -439,12 +447,13 @@ def bench_allreduce(args):
     t_e2e = _max_over_ranks(sum(e2e_t) / len(e2e_t), dev)
 
     # NCCL all_reduce comparator on the same tensor
-    y = x.clone()
-    for _ in range(3):
+    nccl_gbs = nccl_scatter_gbs = None
+    y = x.clone() if not oversub else None
+    for _ in range(3 if not oversub else 0):
         dist.all_reduce(y)
     torch.cuda.synchronize()
     nt = []
-    for _ in range(max(3, min(args.steps, 10))):
+    for _ in range(max(3, min(args.steps, 10)) if not oversub else 0):
         y.copy_(x)
         dist.barrier()
         torch.cuda.synchronize()
@@ -454,7 +463,8 @@ def bench_allreduce(args):
         e1.record(stream)
         torch.cuda.synchronize()
         nt.append(e0.elapsed_time(e1) * 1e-3)
-    nccl_gbs = S_CFG2 / _max_over_ranks(sum(nt) / len(nt), dev) / 1e9
+    if nt:
+        nccl_gbs = round(S_CFG2 / _max_over_ranks(sum(nt) / len(nt), dev) / 1e9, 2)
 
     # configs[2]: binomial-tree compressed Scatter of a 1 GiB root buffer vs NCCL scatter
     ns = (1 << 30) // 4
@@ -479,11 +489,11 @@ def bench_allreduce(args):
     # (NCCL scatter needs equal parts: the largest multiple of N values)
     parts = list(root_buf[: (ns // world) * world].chunk(world)) if rank == 0 else None
     ys = torch.empty(ns // world, dtype=torch.float32, device=dev)
-    for _ in range(3):
+    for _ in range(3 if not oversub else 0):
         dist.scatter(ys, parts, src=0)
     torch.cuda.synchronize()
     nst = []
-    for _ in range(max(3, min(args.steps, 10))):
+    for _ in range(max(3, min(args.steps, 10)) if not oversub else 0):
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = ev(), ev()
@@ -492,7 +502,8 @@ def bench_allreduce(args):
         e1.record(stream)
         torch.cuda.synchronize()
         nst.append(e0.elapsed_time(e1) * 1e-3)
-    nccl_scatter_gbs = 4 * ns / _max_over_ranks(sum(nst) / len(nst), dev) / 1e9
+    if nst:
+        nccl_scatter_gbs = round(4 * ns / _max_over_ranks(sum(nst) / len(nst), dev) / 1e9, 2)
 
     # recursive-doubling allreduce (the paper's gZ-Allreduce(ReDoub)) on the same tensors
     rdo = torch.empty_like(x)
@@ -529,10 +540,10 @@ def bench_allreduce(args):
             "data": "synthetic smooth field per rank (phase 0.37 r)",
             "config": {"workload": "ring-allreduce (compressed RS + compress-once AG), 512 MiB f32 per rank, eb=1e-4",
                        "parallelism": f"ring over {world} GPUs, NVLink peer memory (CUDA IPC)",
-                       "nccl_allreduce_gbs": round(nccl_gbs, 2), "compression_ratio": cr,
+                       "nccl_allreduce_gbs": nccl_gbs, "compression_ratio": cr,
                        "collective_roofline_gbs": round(900.0 * (cr or 1.0), 1),
                        "collective_roofline_frac": round(value / (900.0 * (cr or 1.0)), 4),
-                       "scatter_1GiB_gbs": round(scatter_gbs, 2), "nccl_scatter_1GiB_gbs": round(nccl_scatter_gbs, 2),
+                       "scatter_1GiB_gbs": round(scatter_gbs, 2), "nccl_scatter_1GiB_gbs": nccl_scatter_gbs,
                        "rd_allreduce_gbs": round(rd_gbs, 2),
                        "l2": "inputs (512 MiB) larger than L2"},
             "roofline": {"bound": "hbm", "kernel": "fused RS step = k_tile_encode<STEP> + k_gather",
@@ -545,6 +556,9 @@ def bench_allreduce(args):
             "gpu_launches": launches,
             "clocks": clk.summary(),
         }
+        if oversub:
+            line["rehearsal"] = (f"{world} ranks on {torch.cuda.device_count()} GPUs (time-sliced): "
+                                 "code-path check, not a measurement")
         print(json.dumps(line), flush=True)
     c.close()
     dist.barrier()

@@ -22,9 +22,17 @@ def main():
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # rehearsal of rank counts above the box's GPU count (tools/gpu_n8_rehearsal.sh):
+    # several ranks share a GPU, so NCCL (one rank per GPU) is replaced by gloo for
+    # the object plumbing; the data path is the same CUDA-IPC peer memory
+    oversub = world > torch.cuda.device_count()
+    local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    if oversub:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=dev)
     from oracle import oracle as O
     from paper_2308_05199_b200 import comm
     import golden_data as G
@@ -164,7 +172,7 @@ def main():
         if "sum" not in str(err):
             failures.append(f"bad counts message {err}")
     checked += 1
-    flag = torch.tensor([len(failures)], device=dev)
+    flag = torch.tensor([len(failures)], device="cpu" if oversub else dev)
     dist.all_reduce(flag)
     if rank == 0:
         print(f"mgpu ranks={world} checked={checked} failures={int(flag.item())}", flush=True)
