@@ -477,11 +477,12 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(idx_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
+    cudaFuncSetAttribute(idx_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM);
     attr = true;
   }
   idx_chunks<<<(unsigned)nch, 160, csm, s>>>(nseg, iw);
   idx_resolve<<<1, 32, 0, s>>>(nch, iw);
-  idx_emit<<<(unsigned)nch, CH, 0, s>>>(payload, payload_len, nseg, n, iw, st);
+  idx_emit<<<(unsigned)((nseg + EG - 1) / EG), CH, EMIT_SMEM, s>>>(payload, payload_len, nseg, n, iw, st);
   if (nblocks(n) > payload_len / 5 + 1) return (int)cudaGetLastError();  // certainly truncated: no sidecar
   const uint64_t nt = ntiles_of(n);
   const uint64_t work = nt + 1;

@@ -113,31 +113,76 @@ __device__ __forceinline__ void idx_error(Status* st, uint64_t blk, int w, unsig
   atomicMin(&st->decode_error, (unsigned long long)((blk << 24) | ((uint64_t)(w & 0xFFFF) << 8) | code));
 }
 
+// One CTA per EG consecutive segments (a chunk is CH / EG CTAs, so the walk is
+// spread over ~nseg / EG SMs instead of one CTA per chunk).  The CTA stages the
+// exit/count maps of its chunk's segments up to its own, and its segments'
+// payload bytes, in shared memory: the entry resolution and the block walk
+// are then chains of shared-memory loads instead of dependent L2 round trips.
+constexpr int EG = 16;
+constexpr size_t EMIT_MAP = ((size_t)(CH - 1) * NE * 2 + 15) & ~(size_t)15;  // one map array, 16-B padded
+constexpr size_t EMIT_SMEM = (size_t)EG * SEG + 2 * EMIT_MAP;
+static_assert(CH % EG == 0, "a chunk is a whole number of emit CTAs");
+
 __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t psize, uint64_t nseg, uint64_t n,
                                                IndexWs ws, Status* st) {
-  __shared__ int s_entry[CH];
-  __shared__ unsigned long long s_base[CH];
-  const uint64_t c = blockIdx.x;
-  const uint64_t s0 = c * CH;
-  const int ns = (int)umin64(CH, nseg - s0);
+  extern __shared__ __align__(16) unsigned char esm[];
+  uint8_t* sbytes = esm;                                          // [EG * SEG]
+  short* sx = reinterpret_cast<short*>(esm + (size_t)EG * SEG);   // [(CH - 1) * NE]
+  unsigned short* sc = reinterpret_cast<unsigned short*>(esm + (size_t)EG * SEG + EMIT_MAP);
+  __shared__ int s_entry[EG];
+  __shared__ unsigned long long s_base[EG];
+  const uint64_t s_first = (uint64_t)blockIdx.x * EG;
+  const uint64_t c = s_first / CH;
+  const uint64_t sc0 = c * CH;
+  const int ns = (int)umin64(EG, nseg - s_first);
+  const int nmap = (int)(s_first - sc0) + ns - 1;  // maps needed: chunk start .. our last segment - 1
   const uint64_t nb = (n + BLOCK - 1) / BLOCK;
   const int last_cnt = (int)(n - (nb - 1) * BLOCK);
+  {  // the maps are 16-B aligned (chunk stride CH * NE * 2 = 33024 B): 16-B loads, many in flight
+    const int nv = nmap * NE * 2 / 16;
+    const uint4* gx = reinterpret_cast<const uint4*>(ws.exit + sc0 * NE);
+    const uint4* gc = reinterpret_cast<const uint4*>(ws.count + sc0 * NE);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      const uint4 a = __ldg(gx + i), b = __ldg(gc + i);
+      reinterpret_cast<uint4*>(sx)[i] = a;
+      reinterpret_cast<uint4*>(sc)[i] = b;
+    }
+    for (int i = nv * 8 + threadIdx.x; i < nmap * NE; i += blockDim.x) {
+      sx[i] = ws.exit[sc0 * NE + i];
+      sc[i] = ws.count[sc0 * NE + i];
+    }
+  }
+  const uint64_t g0 = s_first * SEG;
+  const int len = (int)umin64((uint64_t)ns * SEG, psize > g0 ? psize - g0 : 0);
+  if ((reinterpret_cast<uintptr_t>(payload) & 7) == 0) {
+    const uint2* src = reinterpret_cast<const uint2*>(payload + g0);
+#pragma unroll 8
+    for (int i = threadIdx.x; i < (len >> 3); i += blockDim.x) reinterpret_cast<uint2*>(sbytes)[i] = __ldg(src + i);
+    for (int i = (len & ~7) + threadIdx.x; i < len; i += blockDim.x) sbytes[i] = __ldg(payload + g0 + i);
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) sbytes[i] = __ldg(payload + g0 + i);
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
     long long entry = ws.centry[c];
     unsigned long long base = ws.cbase[c];
-    for (int k = 0; k < ns; ++k) {
-      s_entry[k] = (int)entry;
-      s_base[k] = base;
-      if (entry >= 0) {
-        base += ws.count[(s0 + k) * NE + entry];
-        entry = ws.exit[(s0 + k) * NE + entry];
+    const int kpre = (int)(s_first - sc0);
+    for (int k = 0; k < kpre + ns; ++k) {
+      if (k >= kpre) {
+        s_entry[k - kpre] = (int)entry;
+        s_base[k - kpre] = base;
+      }
+      if (entry >= 0 && k < nmap) {
+        base += sc[k * NE + entry];
+        entry = sx[k * NE + entry];
       }
     }
   }
   __syncthreads();
   const int k = threadIdx.x;
   if (k >= ns) return;
-  const uint64_t s = s0 + k;
+  const uint64_t s = s_first + k;
   int e = s_entry[k];
   if (e == EX_END || e == EX_DEAD || e < 0) {
     // chain never enters this segment: an earlier segment reported the error
@@ -152,7 +197,7 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
       idx_error(st, blk, 0, DE_TRUNC);
       return;
     }
-    const int w = __ldg(payload + pos);
+    const int w = sbytes[pos - g0];  // pos < min(psize, send): staged
     const int cnt = (blk == nb - 1) ? last_cnt : BLOCK;
     int size;
     if (w == RAW_WIDTH) size = 1 + 4 * cnt;  // 310-311

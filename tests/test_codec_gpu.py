@@ -199,3 +199,27 @@ def test_fixed_rate_errors(ws):
         gz.fixed_rate_decompress(blob[:5])
     with pytest.raises(ValueError, match="offset 3"):
         gz.fixed_rate_compress(np.array([0, 1, 2, np.inf], np.float32), 4, ws)
+
+
+def test_index_large_reference_blob_and_deep_errors(oracle, ws):
+    # a multi-chunk reference blob (payload >> 128 segments of 2 KiB) decoded from host
+    # bytes through gz_index, then errors planted deep inside it: the first failing
+    # block in walk order is reported, as in codec.py:298-322
+    n = 3_000_001
+    x = oracle.smooth_field(n) + np.random.default_rng(11).normal(0, 1e-2, n).astype(np.float32)
+    ref, offs = oracle.compress(x, 1e-4, threads=8, return_offsets=True)
+    assert len(ref) > 24 + 300 * 2048
+    y = gz.decompress(ref, ws)
+    assert y.tobytes() == oracle.decompress(ref, threads=8).tobytes()
+    yh = gz.decompress(torch.frombuffer(bytearray(ref), dtype=torch.uint8).pin_memory(), ws)
+    assert yh.numpy().tobytes() == y.tobytes()
+    nb = len(offs)
+    for k in (nb // 3, nb // 2 + 17, nb - 2):
+        bad = bytearray(ref)
+        bad[24 + int(offs[k])] = 77
+        with pytest.raises(gz.DecodeError, match=f"width code 77 at block {k}"):
+            gz.decompress(bytes(bad), ws)
+    with pytest.raises(gz.DecodeError, match="truncated"):
+        gz.decompress(ref[:-5], ws)
+    with pytest.raises(gz.DecodeError, match="trailing"):
+        gz.decompress(ref + b"\x00\x00", ws)
