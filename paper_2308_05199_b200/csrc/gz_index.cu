@@ -40,11 +40,18 @@ struct IndexWs {
 __device__ __forceinline__ int full_size(int w) { return w == RAW_WIDTH ? 1 + 4 * BLOCK : 5 + (31 * w + 7) / 8; }
 
 __global__ void __launch_bounds__(160) idx_segments(const uint8_t* payload, uint64_t psize, IndexWs ws) {
-  __shared__ uint8_t seg[SEG];
+  __shared__ __align__(16) uint8_t seg[SEG];
   const uint64_t s = blockIdx.x;
   const uint64_t g0 = s * SEG;
   const int len = (int)umin64(SEG, psize - g0);
-  for (int i = threadIdx.x; i < len; i += blockDim.x) seg[i] = __ldg(payload + g0 + i);
+  if ((reinterpret_cast<uintptr_t>(payload) & 7) == 0) {  // 8-B loads, all in flight at once
+    const uint2* src = reinterpret_cast<const uint2*>(payload + g0);
+#pragma unroll 2
+    for (int i = threadIdx.x; i < (len >> 3); i += blockDim.x) reinterpret_cast<uint2*>(seg)[i] = __ldg(src + i);
+    for (int i = (len & ~7) + threadIdx.x; i < len; i += blockDim.x) seg[i] = __ldg(payload + g0 + i);
+  } else {
+    for (int i = threadIdx.x; i < len; i += blockDim.x) seg[i] = __ldg(payload + g0 + i);
+  }
   __syncthreads();
   const int e = threadIdx.x;
   if (e >= NE) return;
@@ -72,15 +79,26 @@ __global__ void __launch_bounds__(160) idx_segments(const uint8_t* payload, uint
 }
 
 __global__ void __launch_bounds__(160) idx_chunks(uint64_t nseg, IndexWs ws) {
-  extern __shared__ unsigned char sm[];
+  extern __shared__ __align__(16) unsigned char sm[];
   short* sx = reinterpret_cast<short*>(sm);
   unsigned short* sc = reinterpret_cast<unsigned short*>(sm + CH * NE * sizeof(short));
   const uint64_t c = blockIdx.x;
   const uint64_t s0 = c * CH;
   const int ns = (int)umin64(CH, nseg - s0);
-  for (int i = threadIdx.x; i < ns * NE; i += blockDim.x) {
-    sx[i] = ws.exit[s0 * NE + i];
-    sc[i] = ws.count[s0 * NE + i];
+  {  // chunk maps are 16-B aligned (stride CH * NE * 2 = 33024 B): 16-B loads
+    const int nv = ns * NE * 2 / 16;
+    const uint4* gx = reinterpret_cast<const uint4*>(ws.exit + s0 * NE);
+    const uint4* gc = reinterpret_cast<const uint4*>(ws.count + s0 * NE);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      const uint4 a = __ldg(gx + i), b = __ldg(gc + i);
+      reinterpret_cast<uint4*>(sx)[i] = a;
+      reinterpret_cast<uint4*>(sc)[i] = b;
+    }
+    for (int i = nv * 8 + threadIdx.x; i < ns * NE; i += blockDim.x) {
+      sx[i] = ws.exit[s0 * NE + i];
+      sc[i] = ws.count[s0 * NE + i];
+    }
   }
   __syncthreads();
   const int e = threadIdx.x;
