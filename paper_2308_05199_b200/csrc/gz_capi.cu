@@ -478,10 +478,15 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   if (!attr) {
     cudaFuncSetAttribute(idx_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
     cudaFuncSetAttribute(idx_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM);
+    cudaFuncSetAttribute(idx_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RESOLVE_SMEM_MAX);
     attr = true;
   }
   idx_chunks<<<(unsigned)nch, 160, csm, s>>>(nseg, iw);
-  idx_resolve<<<1, 32, 0, s>>>(nch, iw);
+  {
+    const size_t rsm = resolve_smem(nch);
+    const int staged = rsm <= RESOLVE_SMEM_MAX;
+    idx_resolve<<<1, staged ? 512 : 32, staged ? rsm : 0, s>>>(nch, iw, staged);
+  }
   idx_emit<<<(unsigned)((nseg + EG - 1) / EG), CH, EMIT_SMEM, s>>>(payload, payload_len, nseg, n, iw, st);
   if (nblocks(n) > payload_len / 5 + 1) return (int)cudaGetLastError();  // certainly truncated: no sidecar
   const uint64_t nt = ntiles_of(n);

@@ -113,7 +113,25 @@ __global__ void __launch_bounds__(160) idx_chunks(uint64_t nseg, IndexWs ws) {
   ws.ccount[c * NE + e] = tot;
 }
 
-__global__ void idx_resolve(uint64_t nchunk, IndexWs ws) {
+// Serial walk over the chunk maps.  When they fit (RESOLVE_SMEM_MAX), the CTA
+// first copies them into shared memory with coalesced loads, so the walk is a
+// chain of shared-memory loads instead of dependent L2 round trips.
+constexpr size_t RESOLVE_SMEM_MAX = 192 * 1024;
+__host__ __device__ constexpr size_t resolve_smem(uint64_t nchunk) {
+  return nchunk * NE * 4 + ((nchunk * NE * 2 + 15) & ~(uint64_t)15);
+}
+
+__global__ void idx_resolve(uint64_t nchunk, IndexWs ws, int staged) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  unsigned* scc = reinterpret_cast<unsigned*>(rsm);
+  short* sce = reinterpret_cast<short*>(rsm + nchunk * NE * 4);
+  if (staged) {
+    for (uint64_t i = threadIdx.x; i < nchunk * NE; i += blockDim.x) {
+      scc[i] = ws.ccount[i];
+      sce[i] = ws.cexit[i];
+    }
+    __syncthreads();
+  }
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   long long entry = 0;
   unsigned long long base = 0;
@@ -121,8 +139,8 @@ __global__ void idx_resolve(uint64_t nchunk, IndexWs ws) {
     ws.centry[c] = entry;
     ws.cbase[c] = base;
     if (entry < 0) continue;
-    base += ws.ccount[c * NE + entry];
-    entry = ws.cexit[c * NE + entry];
+    base += staged ? scc[c * NE + entry] : ws.ccount[c * NE + entry];
+    entry = staged ? sce[c * NE + entry] : ws.cexit[c * NE + entry];
   }
 }
 
