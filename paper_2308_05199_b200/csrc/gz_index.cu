@@ -41,6 +41,7 @@ __device__ __forceinline__ int full_size(int w) { return w == RAW_WIDTH ? 1 + 4 
 
 __global__ void __launch_bounds__(160) idx_segments(const uint8_t* payload, uint64_t psize, IndexWs ws) {
   __shared__ __align__(16) uint8_t seg[SEG];
+  __shared__ unsigned char ssize[256];
   const uint64_t s = blockIdx.x;
   const uint64_t g0 = s * SEG;
   const int len = (int)umin64(SEG, psize - g0);
@@ -52,28 +53,26 @@ __global__ void __launch_bounds__(160) idx_segments(const uint8_t* payload, uint
   } else {
     for (int i = threadIdx.x; i < len; i += blockDim.x) seg[i] = __ldg(payload + g0 + i);
   }
+  for (int w = threadIdx.x; w < 256; w += blockDim.x)  // full block size per width byte, 0 = invalid
+    ssize[w] = (unsigned char)((w <= 32 || w == RAW_WIDTH) ? full_size(w) : 0);
   __syncthreads();
   const int e = threadIdx.x;
   if (e >= NE) return;
   int p = e, cnt = 0;
-  short ex;
-  while (true) {
-    if (p >= SEG) {
-      ex = (short)(p - SEG);
+  short ex = 0;
+  bool dead = false;
+  while (p < len) {  // len <= SEG
+    const int sz = ssize[seg[p]];
+    if (sz == 0) {
+      dead = true;
       break;
     }
-    if (p >= len) {  // the payload ends inside this segment
-      ex = EX_END;
-      break;
-    }
-    const int w = seg[p];
-    if (w > 32 && w != RAW_WIDTH) {
-      ex = EX_DEAD;
-      break;
-    }
-    p += full_size(w);
+    p += sz;
     ++cnt;
   }
+  if (dead) ex = EX_DEAD;
+  else if (p >= SEG) ex = (short)(p - SEG);
+  else ex = EX_END;  // the payload ends inside this segment
   ws.exit[s * NE + e] = ex;
   ws.count[s * NE + e] = (unsigned short)cnt;
 }
