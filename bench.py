@@ -232,8 +232,14 @@ def bench_codec(args):
             td.append(e1.elapsed_time(e2) * 1e-3)
     torch.cuda.synchronize()
     launches = int(lib.gz_launch_count()) - launches0
-    # parity of the timed output against the oracle-pinned first blob
-    assert bytes(out[:Lb].cpu().numpy().tobytes()) == bytes(blob0), "timed blob differs"
+    # parity (outside the timed region): the blob of the LAST timed call and its decoded
+    # values are byte-compared with the CPU oracle (C restatement of codec.py, all host threads)
+    thr_all = cpu_threads()
+    ref_blob = O.compress(xh, EB, threads=thr_all)
+    assert int(ws.status[4].item()) == len(ref_blob), "timed blob length differs from the oracle"
+    assert out[:Lb].cpu().numpy().tobytes() == ref_blob, "timed blob differs from the oracle"
+    assert y.cpu().numpy().tobytes() == O.decompress(ref_blob, threads=thr_all).tobytes(), "decode differs"
+    parity = {"cfg1": "bit-exact vs oracle (blob + decoded values of the last timed step)"}
     t_c, t_d = sum(tc) / len(tc), sum(td) / len(td)
     bytes_c = 4 * n + Lb
     bytes_d = Lb + 4 * n
@@ -280,6 +286,11 @@ def bench_codec(args):
             tcb.append(e0.elapsed_time(e1) * 1e-3)
             tdb.append(e1.elapsed_time(e2) * 1e-3)
         tcb_m, tdb_m = sorted(tcb)[len(tcb) // 2], sorted(tdb)[len(tdb) // 2]
+        refb = O.compress(xb.cpu().numpy(), EB, threads=cpu_threads())
+        assert Lbb == len(refb) and outb[:Lbb].cpu().numpy().tobytes() == refb, "2^27 blob differs from the oracle"
+        assert yb_.cpu().numpy().tobytes() == O.decompress(refb, threads=cpu_threads()).tobytes(), "2^27 decode differs"
+        parity["codec_2p27"] = "bit-exact vs oracle"
+        del refb
         big = {"values": nb, "compressed_bytes": Lbb, "compress_us": round(tcb_m * 1e6, 1),
                "decompress_us": round(tdb_m * 1e6, 1),
                "compress_hbm_gbs": round((4 * nb + Lbb) / tcb_m / 1e9, 1),
@@ -287,6 +298,8 @@ def bench_codec(args):
                "decompress_hbm_gbs": round((4 * nb + Lbb) / tdb_m / 1e9, 1),
                "decompress_frac": round((4 * nb + Lbb) / tdb_m / 1e9 / peak, 4), "stat": "median"}
         del xb, outb, scb, twsb, yb_
+    except AssertionError:
+        raise
     except Exception as e:  # a supplementary number must not sink the line
         big = {"error": str(e)[:200]}
 
@@ -339,6 +352,7 @@ def bench_codec(args):
                 "wall_ms_per_step": round(sum(e2e_t) / len(e2e_t) * 1e3, 3)},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "parity": parity,
     }
     print(json.dumps(line), flush=True)
     return 0

@@ -41,8 +41,11 @@ typedef struct gz_status {
   uint64_t decode_error;    /* (block_index << 24) | (width << 8) | code, ~0 if none; the smallest
                                block index wins; codes 1 width, 2 truncated, 3 trailing bytes,
                                4 sidecar mismatch, 5 header (codec.py:273-322) */
-  uint64_t reserved[2];
+  uint64_t trailing_bytes;  /* trailing byte count of a code-3 decode error (codec.py:321-322) */
+  uint64_t comm_error;      /* 1: a peer flag never arrived (in-kernel wait gave up after
+                               GZ_FLAG_TIMEOUT_NS; the kernel skipped its work), ~0 if none */
 } gz_status;
+#define GZ_FLAG_TIMEOUT_NS 20000000000ull
 
 /* ---- sizing (host functions, no device work) ---------------------------- */
 /* Compressed-size bound incl. header and 64 B of read slack.  Tighter than
@@ -132,7 +135,12 @@ typedef struct {
                           IPC-mapped) once the whole output is written -- a fused gz_stream_write_u32 */
   uint32_t* wait_flag; /* slotted output only, may be NULL: the kernel waits until this (own-memory) flag
                           is >= 1 before reading its inputs and resets it to 0 when done -- a fused
-                          wait + reset (bounded: traps after ~20 s) */
+                          wait + reset.  Bounded: after GZ_FLAG_TIMEOUT_NS the kernel records
+                          comm_error = 1 in d_status, skips its work and still posts post_flag, so
+                          the peers' streams drain instead of hanging */
+  uint64_t report_base; /* added to the offset of a non-finite value of `local` before it is recorded
+                           in d_status->first_nonfinite (the chunk's offset in the caller's buffer,
+                           so the first bad offset of the whole buffer is reported, codec.py:79-86) */
 } gz_step_io;
 uint64_t gz_slots_bytes(uint64_t m);
 int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,
@@ -148,8 +156,11 @@ int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double 
 uint64_t gz_segments_workspace_bytes(const uint64_t* h_counts, uint32_t nseg);
 int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,
                          const uint64_t* h_seg_blob_off, uint64_t* d_seg_len, void* sidecars,
-                         const uint64_t* h_seg_sidecar_off, void* ws, uint64_t ws_bytes, gz_status* d_status,
-                         gz_stream_t stream);
+                         const uint64_t* h_seg_sidecar_off, const uint64_t* h_seg_report_off, void* ws,
+                         uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream);
+/*   h_seg_report_off (may be NULL): per segment, the offset of its first value
+ *   in the caller's buffer, added to a non-finite offset before it is recorded
+ *   (NULL: the segment's offset inside x). */
 
 /* ---- peer memory (CUDA IPC over NVLink) ----------------------------------- */
 int gz_ipc_handle_size(void);
@@ -185,6 +196,12 @@ typedef struct {
   uint64_t max_bytes;
 } gz_copy_item;
 #define GZ_MAX_COPY_ITEMS 64
+/* dst[n] = src[n] (f32, 16-byte aligned) recording the first non-finite offset
+ * (+ report_base) in d_status->first_nonfinite (codec.py:79-86): the parts of a
+ * collective's input that are kept verbatim, never compressed (the scatter
+ * root's own block, collectives.py:500), are validated like the rest. */
+int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_base, gz_status* d_status,
+                    gz_stream_t stream);
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream);
 /* the same on at most sms_budget SMs (0: all), so that it can run beside a
  * decoder launched with reserve_sms = sms_budget (allgather pipeline) */
@@ -192,11 +209,14 @@ int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget,
 
 /* ---- fixed-rate baseline codec (codec.py:442-489, a comparator) --------------
  * Uniform quantisation of the whole buffer over [min, max] to `bits` (1..16)
- * per value, "<QBff" header (n, bits, lo, hi) + codes LSB-first.  ws8: 8 bytes
- * of device scratch.  The host validates a blob's header before decoding. */
+ * per value, "<QBff" header (n, bits, lo, hi) + codes LSB-first.  ws:
+ * gz_fr_workspace_bytes() of device scratch.  A zero min / max carries the
+ * sign numpy's AVX-512 reduction returns (x.min() / x.max(), codec.py:454-455).
+ * The host validates a blob's header before decoding. */
 uint64_t gz_fr_bound(uint64_t n, uint32_t bits);
+uint64_t gz_fr_workspace_bytes(void);
 int gz_fr_compress(const float* x, uint64_t n, uint32_t bits, uint8_t* out, uint64_t out_cap, uint64_t* d_len,
-                   void* ws8, gz_status* d_status, gz_stream_t stream);
+                   void* ws, gz_status* d_status, gz_stream_t stream);
 int gz_fr_decompress(const uint8_t* blob, uint64_t n, uint32_t bits, float* y, gz_stream_t stream);
 
 /* number of kernels this library has launched so far (all entry points) */

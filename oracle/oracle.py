@@ -302,8 +302,9 @@ def pack_scatter_msg(sizes, lo, hi, frag: bytes) -> bytes:
     return _SC_HDR.pack(len(sizes), lo, hi) + np.asarray(sizes, dtype="<u8").tobytes() + frag
 
 
-def binomial_scatter(data, N, eb, root=0, counts=None, trace=None):
-    """binomial_scatter_c, collectives.py:467-532 (messages appended to trace)."""
+def binomial_scatter(data, N, eb, root=0, counts=None, trace=None, threads=1):
+    """binomial_scatter_c, collectives.py:467-532 (messages appended to trace;
+    threads: host threads per codec call)."""
     data = np.ascontiguousarray(data, "<f4").reshape(-1)
     if counts is None:
         counts = [hi - lo for lo, hi in chunk_spans(data.size, N)]
@@ -317,7 +318,7 @@ def binomial_scatter(data, N, eb, root=0, counts=None, trace=None):
     if N == 1:
         return outputs
     order = [(root + j) % N for j in range(N)]
-    blobs = [compress(slices[r], eb) for r in order]
+    blobs = [compress(slices[r], eb, threads=threads) for r in order]
     sizes = [len(b) for b in blobs]
     offs = np.concatenate([[0], np.cumsum(sizes)]).astype(int)
     payload = b"".join(blobs)
@@ -341,7 +342,7 @@ def binomial_scatter(data, N, eb, root=0, counts=None, trace=None):
             if trace is not None:
                 trace.append((me, order[child], cmsg))
         own = frag[offs[vr] - offs[lo] : offs[vr] + sizes[vr] - offs[lo]]
-        outputs[me] = decompress(own)
+        outputs[me] = decompress(own, threads=threads)
     return outputs
 
 
@@ -357,6 +358,37 @@ def smooth_field(n: int, phase: float = 0.0) -> np.ndarray:
 FR_HEADER_BYTES = 17  # struct "<QBff": n, bits, lo, hi
 
 
+def np_extremum_avx512(x: np.ndarray, op: str) -> float:
+    """x.min() / x.max() of a contiguous float32 array exactly as numpy 2.x
+    computes it on an AVX-512 host (the host the reference's goldens were made
+    on), INCLUDING the sign of a zero result, which numpy's SIMD reduction
+    makes order-dependent (codec.py:454-455 calls x.min() / x.max()):
+    numpy's simd_reduce_c (loops_minmax.dispatch.c.src) starts 16 lanes at
+    x[0], folds x[1 + 16j + l] into lane l with vminps / vmaxps (a tie returns
+    the SECOND operand), combines the lanes with GCC's _mm512_reduce_min_ps /
+    _mm512_reduce_max_ps tree and folds the (n-1) % 16 tail values in one by
+    one (ties again return the later value).  Pure Python, for small inputs."""
+    x = np.ascontiguousarray(x, "<f4").reshape(-1)
+    better = (lambda a, b: a < b) if op == "min" else (lambda a, b: a > b)
+
+    def f(a, b):  # (value, index); the first operand only wins a strict comparison
+        return a if better(a[0], b[0]) else b
+
+    n = x.size
+    nv = (n - 1) // 16
+    lane = [(float(x[0]), 0)] * 16
+    for j in range(nv):
+        for l in range(16):
+            i = 1 + 16 * j + l
+            lane[l] = f(lane[l], (float(x[i]), i))
+    t3 = [f(lane[8 + i], lane[i]) for i in range(8)]
+    t6 = [f(t3[4 + i], t3[i]) for i in range(4)]
+    r = f(f(t6[0], t6[2]), f(t6[1], t6[3]))
+    for i in range(1 + 16 * nv, n):
+        r = f(r, (float(x[i]), i))
+    return float(x[r[1]])
+
+
 def fixed_rate_compress(data, bits_per_value: int) -> bytes:
     import struct
 
@@ -367,6 +399,11 @@ def fixed_rate_compress(data, bits_per_value: int) -> bytes:
     n = x.size
     lo = float(x.min()) if n else 0.0
     hi = float(x.max()) if n else 0.0
+    # a zero extremum's sign is order-dependent in numpy: follow the AVX-512 reduction
+    if n and lo == 0.0:
+        lo = np_extremum_avx512(x, "min") if n < 100_000 else _zero_sign_fast(x, lo)
+    if n and hi == 0.0:
+        hi = np_extremum_avx512(x, "max") if n < 100_000 else _zero_sign_fast(x, hi)
     head = struct.pack("<QBff", n, b, lo, hi)
     if n == 0:
         return head
@@ -379,6 +416,34 @@ def fixed_rate_compress(data, bits_per_value: int) -> bytes:
         q = np.zeros(n, dtype=np.uint32)
     bitsarr = ((q[:, None] >> np.arange(b, dtype=np.uint32)[None, :]) & 1).astype(np.uint8).reshape(-1)
     return head + np.packbits(bitsarr, bitorder="little").tobytes()
+
+
+def _zero_sign_fast(x: np.ndarray, v: float) -> float:
+    """np_extremum_avx512 for a zero extremum on large inputs (vectorised):
+    the winner is the last zero of the scalar tail, else the lane the GCC
+    reduction tree selects among the lanes whose last zero exists."""
+    n = x.size
+    nv = (n - 1) // 16
+    tail = np.flatnonzero(x[1 + 16 * nv:] == 0.0)
+    if tail.size:
+        return float(x[1 + 16 * nv + tail[-1]])
+    last = [-1] * 16
+    if nv:
+        body = x[1:1 + 16 * nv].reshape(nv, 16) == 0.0
+        for l in range(16):
+            z = np.flatnonzero(body[:, l])
+            if z.size:
+                last[l] = 1 + 16 * int(z[-1]) + l
+    x0z = x[0] == 0.0
+    lane = [last[l] if last[l] >= 0 else (0 if x0z else -1) for l in range(16)]
+
+    def f(a, b):
+        return b if b >= 0 else a
+
+    t3 = [f(lane[8 + i], lane[i]) for i in range(8)]
+    t6 = [f(t3[4 + i], t3[i]) for i in range(4)]
+    r = f(f(t6[0], t6[2]), f(t6[1], t6[3]))
+    return float(x[r]) if r >= 0 else v
 
 
 def fixed_rate_decompress(blob) -> np.ndarray:

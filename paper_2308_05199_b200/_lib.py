@@ -36,7 +36,7 @@ SIGNATURES = {
     "gz_index_workspace_bytes": (u64, [u64]),
     "gz_reduce_step": (i32, [p, p, p, u64, dbl, i32, p, p, u64, p, p, p, u64, p, p]),
     "gz_segments_workspace_bytes": (u64, [p, u32]),
-    "gz_compress_segments": (i32, [p, p, u32, dbl, p, p, p, p, p, p, u64, p, p]),
+    "gz_compress_segments": (i32, [p, p, u32, dbl, p, p, p, p, p, p, p, u64, p, p]),
     "gz_ipc_handle_size": (i32, []),
     "gz_ipc_get_handle": (i32, [p, p]),
     "gz_ipc_open_handle": (i32, [p, ctypes.POINTER(ctypes.c_void_p)]),
@@ -47,6 +47,7 @@ SIGNATURES = {
     "gz_stream_flag_ops": (i32, [p, p, u32]),
     "gz_copy_blob": (i32, [p, p, p, u64, p]),
     "gz_copy_items": (i32, [p, u32, p]),
+    "gz_copy_checked": (i32, [p, p, u64, u64, p, p]),
     "gz_copy_items_sms": (i32, [p, u32, i32, p]),
     "gz_launch_count": (u64, []),
     "gz_debug_stamp": (i32, [p, p]),
@@ -54,6 +55,7 @@ SIGNATURES = {
     "gz_step": (i32, [p, p, u64, dbl, i32, p, p, u64, p, p]),
     "gz_step_reduce": (i32, [p, p, u64, dbl, i32, p, p, p]),
     "gz_fr_bound": (u64, [u64, u32]),
+    "gz_fr_workspace_bytes": (u64, []),
     "gz_fr_compress": (i32, [p, u64, u32, p, u64, p, p, p, p]),
     "gz_fr_decompress": (i32, [p, u64, u32, p, p]),
 }

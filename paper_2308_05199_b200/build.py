@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgzccl.so")
 SOURCES = ["gz_capi.cu"]
-DEPS = ["gz_capi.cu", "gz_codec.cu", "gz_device.cuh", "gz_index.cu", "gz_comm.cu", "../../include/gzccl.h"]
+DEPS = ["gz_capi.cu", "gz_codec.cu", "gz_device.cuh", "gz_index.cu", "gz_fixed.cu", "../../include/gzccl.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

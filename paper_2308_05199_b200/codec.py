@@ -250,7 +250,7 @@ def _decode_with_sidecar(blob_dev: torch.Tensor, sidecar: torch.Tensor, n: int, 
     return y
 
 
-def index(blob_dev: torch.Tensor, n: int, payload_len: int, ws: Workspace, stream=None) -> torch.Tensor:
+def build_sidecar(blob_dev: torch.Tensor, n: int, payload_len: int, ws: Workspace, stream=None) -> torch.Tensor:
     """Build the device sidecar of a reference blob, validating it like codec.py:298-322."""
     lib = L.lib()
     sidecar = torch.empty(int(lib.gz_sidecar_bytes(n)), dtype=torch.uint8, device=blob_dev.device)
@@ -285,7 +285,7 @@ def decompress(blob, workspace: Workspace | None = None, *, stream=None, check: 
         ws = _ws_for(workspace, dev)
         buf = ws.get("decompress.blob", total + 64)
         buf[:total].copy_(hb, non_blocking=True)
-        sidecar = index(buf, n, total - HEADER_BYTES, ws, stream)
+        sidecar = build_sidecar(buf, n, total - HEADER_BYTES, ws, stream)
         y = _decode_with_sidecar(buf, sidecar, n, eb, ws, stream, check)
         out = torch.empty(n, dtype=torch.float32, pin_memory=True)
         out.copy_(y, non_blocking=True)
@@ -316,7 +316,7 @@ def decompress(blob, workspace: Workspace | None = None, *, stream=None, check: 
         buf[:total].copy_(src.reshape(-1))
     else:
         buf[:total].copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
-    sidecar = index(buf, n, payload_len, ws, stream)
+    sidecar = build_sidecar(buf, n, payload_len, ws, stream)
     y = _decode_with_sidecar(buf, sidecar, n, eb, ws, stream, check)
     return y if on_dev else y.cpu().numpy()
 
@@ -385,19 +385,19 @@ def compress_blocks(data, counts, eb, workspace: Workspace | None = None):
     return seg.packed_bytes(), table
 
 
-def decompress_block(payload, table: BlockTable, index_: int, workspace: Workspace | None = None):
+def decompress_block(payload, table: BlockTable, index: int, workspace: Workspace | None = None):
     """Decode one block of a packed payload, touching only that block's bytes (codec.py:430-439)."""
-    if not 0 <= index_ < table.count:
-        raise IndexError(f"block index {index_} out of range [0, {table.count})")
-    off = table.offsets[index_]
-    end = off + table.sizes[index_]
+    if not 0 <= index < table.count:
+        raise IndexError(f"block index {index} out of range [0, {table.count})")
+    off = table.offsets[index]
+    end = off + table.sizes[index]
     if isinstance(payload, torch.Tensor) and payload.is_cuda:
         if end > payload.numel():
-            raise DecodeError(f"payload shorter than block {index_} extent")
+            raise DecodeError(f"payload shorter than block {index} extent")
         return decompress(payload[off:end], workspace)
     payload = bytes(payload)
     if end > len(payload):
-        raise DecodeError(f"payload shorter than block {index_} extent")
+        raise DecodeError(f"payload shorter than block {index} extent")
     return decompress(payload[off:end], workspace)
 
 
@@ -419,7 +419,7 @@ def fixed_rate_compress(data, bits_per_value: int, workspace: Workspace | None =
     lib = L.lib()
     cap = int(lib.gz_fr_bound(n, b))
     out = torch.empty(cap, dtype=torch.uint8, device=x.device)
-    scratch = ws.tile_ws(16)
+    scratch = ws.get("fixed_rate.scratch", int(lib.gz_fr_workspace_bytes()))
     ws.reset_status(stream)
     L.check(lib.gz_fr_compress(x.data_ptr(), n, b, out.data_ptr(), cap, ws.len_ptr(), scratch.data_ptr(),
                                ws.status_ptr(), _stream(stream)), "gz_fr_compress")

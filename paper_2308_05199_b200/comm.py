@@ -41,6 +41,7 @@ from .collectives import _check_op, chunk_spans, scatter_counts
 from .schedule import Compress, Reduce, ring_allreduce_plan
 
 _ALIGN = 256
+_MAX_DECODE_SEGMENTS = 8  # GZ_MAX_DECODE_SEGMENTS (include/gzccl.h)
 AG_COPY_SMS = 24  # SMs left to the allgather's NVLink pulls while the previous owner's blob is decoded
 AG_MULTI_MAX = 8 << 20  # chunk values up to which the allgather decodes every owner in one remote-read launch
 
@@ -109,7 +110,12 @@ class Communicator:
         self.rank = dist.get_rank(self.group)
         self.world = dist.get_world_size(self.group)
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.ws = Workspace(self.device)
+        self.ws = Workspace(self.device)  # status record + tile workspace of rd / scatter
+        # the ring's own tile workspace: sized once per _setup, so the raw pointer a
+        # captured ring graph holds can never be freed by another collective growing
+        # its workspace (the graph cache is cleared whenever _setup reallocates)
+        self._ring_ws = Workspace(self.device)
+        self.flag_timeout_s = 60.0  # host-side bound on check()/synchronize() waits
         self.stream = torch.cuda.current_stream(self.device)
         self.epoch = 0
         self._n = None
@@ -165,6 +171,7 @@ class Communicator:
         flags[self.layout.rs_consumed() // 4] = 1
         for j in range(self.world):
             flags[self.layout.ag_consumed(j) // 4] = 1
+        self._ring_ws.tile_ws(int(lib.gz_workspace_bytes(m_max)))  # allocated (and zeroed) before any capture
         torch.cuda.synchronize(self.device)
         self._n = m_max
         self.epoch = 0
@@ -250,20 +257,31 @@ class Communicator:
             self.events.append((label, ev))
 
     # ------------------------------------------------------------ collectives
-    def ring_allreduce(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
+    def ring_allreduce(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None,
+                       check: bool = True):
         """Per-rank ring_allreduce_c (collectives.py:294-308) on this GPU.
 
         Returns this rank's output: its own reduced chunk (i+1) mod N exact, all
         other chunks decoded from their owners' compress-once blobs.
+
+        Errors (codec.py:79-86 / 273-322) are detected on the device by the
+        kernels that read the data.  ``check=True`` waits for the call (bounded
+        by ``flag_timeout_s``) and raises on every rank the error the reference
+        would raise: ``ValueError("non-finite value at offset k")`` for the
+        first bad value in rank order.  ``check=False`` leaves the call
+        asynchronous; the next :meth:`check` reports its errors.
         """
         x = self._check_input(x)
+        ebf, opc = _check_eb(eb), _check_op(op)
         if out is None:
             out = torch.empty_like(x)
         if self.world == 1:
-            out.copy_(x)
-            return out
-        spans = chunk_spans(x.numel(), self.world)
-        self._run_graphed("allreduce", x, spans, _check_eb(eb), _check_op(op), out)
+            self._copy_checked(x, out)
+        else:
+            spans = chunk_spans(x.numel(), self.world)
+            self._run_graphed("allreduce", x, spans, ebf, opc, out)
+        if check:
+            self.check()
         return out
 
     def _run_graphed(self, mode, x, spans, ebf, opc, out):
@@ -292,27 +310,33 @@ class Communicator:
         self._last_key = key
         self._ring(mode, x, spans, ebf, opc, out)
 
-    def ring_reduce_scatter(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None):
+    def ring_reduce_scatter(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None,
+                            check: bool = True):
         """Per-rank ring_reduce_scatter_c (collectives.py:258-291): returns the
         fully reduced chunk (rank + 1) mod N of chunk_spans(n, N).  The last step
-        decodes and reduces without re-compressing (gz_decompress_reduce)."""
+        decodes and reduces without re-compressing (gz_decompress_reduce).
+        ``check`` as in :meth:`ring_allreduce`."""
         x = self._check_input(x)
+        ebf, opc = _check_eb(eb), _check_op(op)
         N, i = self.world, self.rank
         spans = chunk_spans(x.numel(), N)
         lo, hi = spans[(i + 1) % N]
         if out is None:
             out = torch.empty(hi - lo, dtype=torch.float32, device=self.device)
         if N == 1:
-            out.copy_(x)
-            return out
-        self._run_graphed("reduce_scatter", x, spans, _check_eb(eb), _check_op(op), out)
+            self._copy_checked(x, out)
+        else:
+            self._run_graphed("reduce_scatter", x, spans, ebf, opc, out)
+        if check:
+            self.check()
         return out
 
-    def ring_allgather(self, chunk: torch.Tensor, eb: float, out: torch.Tensor | None = None):
+    def ring_allgather(self, chunk: torch.Tensor, eb: float, out: torch.Tensor | None = None, check: bool = True):
         """Per-rank ring_allgather_c (collectives.py:247-255), allgatherv: every
         rank contributes a chunk of any length; each rank compresses its chunk
         once and the others decode those bytes; the own chunk is kept verbatim.
-        Returns the concatenation in rank order."""
+        Returns the concatenation in rank order.  ``check`` as in
+        :meth:`ring_allreduce`."""
         chunk = self._check_input(chunk)
         ebf = _check_eb(eb)
         N = self.world
@@ -322,14 +346,81 @@ class Communicator:
         if out is None:
             out = torch.empty(total, dtype=torch.float32, device=self.device)
         if N == 1:
-            out.copy_(chunk)
-            return out
-        lo = [0]
-        for c in counts:
-            lo.append(lo[-1] + c)
-        spans = [(lo[r], lo[r + 1]) for r in range(N)]
-        self._ring("allgather", chunk, spans, ebf, 0, out)
+            self._copy_checked(chunk, out)
+        else:
+            lo = [0]
+            for c in counts:
+                lo.append(lo[-1] + c)
+            spans = [(lo[r], lo[r + 1]) for r in range(N)]
+            self._ring("allgather", chunk, spans, ebf, 0, out)
+        if check:
+            self.check()
         return out
+
+    # ------------------------------------------------------------ errors
+    def _copy_checked(self, src: torch.Tensor, dst: torch.Tensor, report_base: int = 0, reset: bool = True):
+        """dst = src on the device, recording the first non-finite offset."""
+        s = torch.cuda.current_stream(self.device).cuda_stream
+        if reset:
+            self.ws.reset_status()
+        if src.numel():
+            L.check(L.lib().gz_copy_checked(src.data_ptr(), dst.data_ptr(), src.numel(), report_base,
+                                            self.ws.status_ptr(), s), "gz_copy_checked")
+
+    def _bounded_sync(self, what: str = "collective"):
+        """Wait for this rank's stream, at most ``flag_timeout_s`` seconds.  A
+        peer that never posts its flag leaves a stream-ordered wait pending
+        forever: the flags of our buffers are then forced (from a side stream)
+        so the queued work drains, the communicator is marked broken and
+        TimeoutError is raised instead of hanging the process."""
+        import time
+
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        t0 = time.perf_counter()
+        delay = 1e-5
+        while not ev.query():
+            if time.perf_counter() - t0 > self.flag_timeout_s:
+                self._poison()
+                raise TimeoutError(f"rank {self.rank}: {what} did not complete within {self.flag_timeout_s} s "
+                                   "(a peer never posted its flag); the communicator is unusable")
+            time.sleep(delay)
+            delay = min(delay * 2, 1e-2)
+
+    def _poison(self):
+        side = torch.cuda.Stream(self.device)
+        with torch.cuda.stream(side):
+            for buf in (self._buf, getattr(self, "_sc_buf", None), getattr(self, "_rd_buf", None)):
+                if buf is not None:
+                    nflag = 4 * 64  # every flag area is at the start of its buffer
+                    buf[: min(nflag, buf.numel())].view(torch.int32).fill_(0x3FFFFFFF)
+        self._broken = True
+
+    def check(self):
+        """Wait for the outstanding calls of this rank (bounded) and raise the
+        first error any rank's kernels recorded since the last reset, on every
+        rank alike (the reference raises for the whole collective)."""
+        import numpy as np
+
+        from .codec import DecodeError, _NONE
+
+        if getattr(self, "_broken", False):
+            raise RuntimeError("communicator is unusable after a peer timeout")
+        self._bounded_sync()
+        st = self.ws.status[:4].cpu().numpy().view(np.uint64)
+        mine = [int(v) for v in st]
+        alls = [None] * self.world
+        dist.all_gather_object(alls, mine, group=self.group)
+        for r, v in enumerate(alls):
+            if v[3] != _NONE:
+                raise RuntimeError(f"rank {r}: a peer flag never arrived (in-kernel wait gave up after 20 s)")
+        for r, v in enumerate(alls):  # collectives.py:202-205: the first bad buffer in rank order
+            if v[0] != _NONE:
+                raise ValueError(f"non-finite value at offset {v[0]}")
+        for r, v in enumerate(alls):
+            if v[1] != _NONE:
+                e = v[1]
+                raise DecodeError(f"rank {r}: inconsistent compressed stream at block {e >> 24} (code {e & 0xFF})")
 
     def _check_input(self, x):
         if not isinstance(x, torch.Tensor) or x.dim() != 1 or x.dtype != torch.float32 or not x.is_cuda:
@@ -348,7 +439,8 @@ class Communicator:
         cur = torch.cuda.current_stream(self.device)  # (a capture stream while recording a graph)
         s = cur.cuda_stream
         ws = self.ws
-        tws = ws.tile_ws(int(lib.gz_workspace_bytes(m_max)))
+        tws = self._ring_ws.tile_ws(int(lib.gz_workspace_bytes(m_max)))  # no reallocation: sized in _setup
+        ws.reset_status(cur)  # errors of this call only (a memset node when captured)
         e = self.epoch + 1
         right, left = (i + 1) % N, (i - 1) % N
         self.spans = spans
@@ -363,8 +455,9 @@ class Communicator:
             sl, sz, wd = lay.slot_off[k]
             return self._addr(r, sl), self._addr(r, sz), self._addr(r, wd)
 
-        def step(inp, local, n_, acc, out_slot=None, out_blob=None, post=None, wait=None):
+        def step(inp, local, n_, acc, out_slot=None, out_blob=None, post=None, wait=None, base=0):
             io = _StepIO()
+            io.report_base = base  # offset of `local` in x: non-finite inputs are reported like codec.py:79-86
             if inp is not None:
                 io.in_slots, io.in_sizes, io.in_widths = inp
             if out_slot is not None:
@@ -413,7 +506,7 @@ class Communicator:
                     # gather); the right neighbour's fused step reads it in place
                     step(None, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot),
                          post=(p.dst, lay.rs_full(p.slot)),
-                         wait=lay.rs_consumed() if self.kernel_waits else None)
+                         wait=lay.rs_consumed() if self.kernel_waits else None, base=spans[p.chunk][0])
                     launches += 1
                     self._mark("compress")
                 elif isinstance(p, Reduce):
@@ -424,6 +517,7 @@ class Communicator:
                         # decode + reduce into the owned chunk; nothing to re-compress
                         io = _StepIO()
                         io.in_slots, io.in_sizes, io.in_widths = inp
+                        io.report_base = spans[p.chunk][0]
                         L.check(lib.gz_step_reduce(ctypes.byref(io), chunk_ptr(x, p.chunk), msize(p.chunk), ebf,
                                                    opc, out.data_ptr(), ws.status_ptr(), s), "gz_step_reduce")
                         launches += 1
@@ -433,13 +527,14 @@ class Communicator:
                     if not p.last:
                         step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), None, out_slot=slot(i, p.slot + 1),
                              post=(p.dst, lay.rs_full(p.slot + 1)),
-                             wait=lay.rs_full(p.slot) if self.kernel_waits else None)
+                             wait=lay.rs_full(p.slot) if self.kernel_waits else None, base=spans[p.chunk][0])
                         launches += 1
                     else:
                         wait_own_blob_free()  # our own blob is read by every peer in the allgather
                         step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), chunk_ptr(out, p.chunk),
                              out_blob=(self._addr(i, lay.own_off[0]), lay.blob_cap,
-                                       self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1])))
+                                       self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1])),
+                             base=spans[p.chunk][0])
                         launches += 2
                     self._mark("reduce_last" if p.last else "reduce")
                     if p.last:
@@ -484,16 +579,23 @@ class Communicator:
         if len(owners) > 1 and mode == "multi":
             # one launch decodes every owner's blob straight out of its memory
             self._take_all([lay.ag_ready(j) for j in owners], s)
-            k = len(owners)
-            P = ctypes.c_void_p * k
-            blobs = P(*[self._addr(j, lay.own_off[0]) for j in owners])
-            scs = P(*[self._addr(j, lay.own_off[1]) for j in owners])
-            ns = (ctypes.c_uint64 * k)(*[msize(chunk_of(j)) for j in owners])
-            ys = P(*[chunk_ptr(out, chunk_of(j)) for j in owners])
-            L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s), "gz_decompress_multi")
+            nl = 0
+            for g0 in range(0, len(owners), _MAX_DECODE_SEGMENTS):  # one launch per 8 owners
+                grp = owners[g0:g0 + _MAX_DECODE_SEGMENTS]
+                k = len(grp)
+                P = ctypes.c_void_p * k
+                blobs = P(*[self._addr(j, lay.own_off[0]) for j in grp])
+                scs = P(*[self._addr(j, lay.own_off[1]) for j in grp])
+                ns = (ctypes.c_uint64 * k)(*[msize(chunk_of(j)) for j in grp])
+                ys = P(*[chunk_ptr(out, chunk_of(j)) for j in grp])
+                L.check(lib.gz_decompress_multi(blobs, scs, ns, k, ebf, ys, 0, ws.status_ptr(), s),
+                        "gz_decompress_multi")
+                nl += 1
             self._mark("decode")
             self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
-            return 1
+            return nl
+        if mode == "bulk" and len(owners) > _MAX_DECODE_SEGMENTS:
+            mode = "copy"
         if mode == "bulk":
             # pull every owner's blob + sidecar in ONE copy launch (the NVLink ingress is the
             # bound; a decode beside a pull runs barely faster than after it), then decode
@@ -582,7 +684,7 @@ class _StepIO(ctypes.Structure):  # gz_step_io (include/gzccl.h)
                 ("in_sizes", ctypes.c_void_p), ("in_widths", ctypes.c_void_p), ("blob_out", ctypes.c_void_p),
                 ("blob_out_cap", ctypes.c_uint64), ("d_len_out", ctypes.c_void_p), ("sidecar_out", ctypes.c_void_p),
                 ("out_slots", ctypes.c_void_p), ("out_sizes", ctypes.c_void_p), ("out_widths", ctypes.c_void_p),
-                ("post_flag", ctypes.c_void_p), ("wait_flag", ctypes.c_void_p)]
+                ("post_flag", ctypes.c_void_p), ("wait_flag", ctypes.c_void_p), ("report_base", ctypes.c_uint64)]
 
 
 class _FlagOp(ctypes.Structure):  # gz_flag_op (include/gzccl.h)
@@ -653,7 +755,8 @@ def _scatter_close(self):
     self._sc_key = None
 
 
-def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: str = "tree", out=None):
+def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: str = "tree", out=None,
+                     check: bool = True):
     """This rank's part of binomial_scatter_c (collectives.py:467-532).
 
     The root passes its whole buffer ``x`` (other ranks: None); every rank
@@ -670,7 +773,9 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
       straight out of the root's memory (same bytes, same output — on NVSwitch
       all peers are one hop away);
     * the size table never travels separately: lengths sit next to the blobs
-      and the sidecar carries the block offsets.
+      and the sidecar carries the block offsets;
+    * errors as in :meth:`Communicator.ring_allreduce` (``check``): a
+      non-finite root value is reported with its offset in the root buffer.
     """
     from .schedule import scatter_route
 
@@ -698,9 +803,12 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
         out = torch.empty(counts[me], dtype=torch.float32, device=self.device)
     lib = L.lib()
     s = self.stream.cuda_stream
+    self.ws.reset_status()
     if N == 1:
-        out.copy_(x)
+        self._copy_checked(x, out, reset=False)
         self.launches_per_call = 1
+        if check:
+            self.check()
         return out
     order = [(root + j) % N for j in range(N)]  # virtual rank -> actual rank
     vcounts = [counts[order[v]] for v in range(N)]
@@ -739,9 +847,10 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
         ws = self.ws.tile_ws(int(lib.gz_segments_workspace_bytes(h_counts, N - 1)))
         base = self._sc_buf.data_ptr()
         L.check(lib.gz_compress_segments(xv.data_ptr(), h_counts, N - 1, ebf, base, arr(*lay.slot[1:]),
-                                         base + lay.len_off + 8, base, arr(*lay.sc[1:]), ws.data_ptr(), ws.numel(),
+                                         base + lay.len_off + 8, base, arr(*lay.sc[1:]),
+                                         arr(*[lo[order[v]] for v in range(1, N)]), ws.data_ptr(), ws.numel(),
                                          self.ws.status_ptr(), s), "gz_compress_segments")
-        out.copy_(x[lo[me]:lo[me + 1]])
+        self._copy_checked(x[lo[me]:lo[me + 1]], out, report_base=lo[me], reset=False)
         launches += 2 + (root != 0)
         targets = [c for c, _, _ in sends] if routing == "tree" else [j for j in range(N) if j != me]
         for j in targets:
@@ -777,6 +886,8 @@ def binomial_scatter(self, x, eb: float, counts=None, root: int = 0, routing: st
             L.check(lib.gz_stream_write_u32(s, at(root, lay.consumed(me)), e), "gz_stream_write_u32")
     self._sc_epoch = e
     self.launches_per_call = launches
+    if check:
+        self.check()
     return out
 
 
@@ -812,7 +923,7 @@ class _RDLayout:
         return 4 * (self.K + k)
 
 
-def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
+def rd_allreduce(self, x, eb: float, op: str = "sum", out=None, check: bool = True):
     """This rank's part of rd_allreduce_c (collectives.py:349-424) over NVLink.
 
     Whole-buffer exchanges with the partner actual(remapped(i) ^ 2^t).  Every
@@ -832,8 +943,11 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
     N, i = self.world, self.rank
     if out is None:
         out = torch.empty_like(x)
+    self.ws.reset_status()
     if N == 1:
-        out.copy_(x)
+        self._copy_checked(x, out, reset=False)
+        if check:
+            self.check()
         return out
     n = x.numel()
     pof2, r, steps, role, remapped, actual = rd_plan(N)
@@ -894,31 +1008,22 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None):
                                    ws.status_ptr(), s), "gz_step_reduce")
         launches += 1
 
-    if role(i) == "donor":
-        a = i + 1
-        send(0, a)  # 381-386
-        wait(lay.full(K - 1), e)  # 430-435: the absorber's result
-        receive_last(a, K - 1, reduce=False)
-        signal(a, lay.consumed(K - 1))
-    else:
-        part = [actual(remapped(i) ^ (1 << t)) for t in range(steps)]
-        if role(i) == "absorber":
-            wait(lay.full(0), e)  # 389-397, fused with the step-0 compression
-            send(1, part[0], src=i - 1, k_in=0)
-            signal(i - 1, lay.consumed(0))
+    from .schedule import RdRecvLast, RdSend, rd_allreduce_plan
+
+    for p in rd_allreduce_plan(N, i):  # the per-rank plan also run over gloo by the CPU tests
+        if isinstance(p, RdSend):
+            if p.src is not None:
+                wait(lay.full(p.k_in), e)  # the sender posted its message k_in
+            send(p.k, p.dst, src=p.src, k_in=p.k_in)
         else:
-            send(1, part[0])
-        for t in range(steps):  # 399-418
-            wait(lay.full(t + 1), e)
-            if t + 1 < steps:
-                send(t + 2, part[t + 1], src=part[t], k_in=t + 1)
-            elif role(i) == "absorber":
-                send(K - 1, i - 1, src=part[t], k_in=t + 1)  # 420-427: the result goes back to the donor
-            else:
-                receive_last(part[t], t + 1, reduce=True)
-            signal(part[t], lay.consumed(t + 1))
+            wait(lay.full(p.k_in), e)
+            receive_last(p.src, p.k_in, reduce=p.reduce)
+        if p.src is not None:
+            signal(p.src, lay.consumed(p.k_in))  # its message buffer is free again
     self._rd_epoch = e
     self.launches_per_call = launches
+    if check:
+        self.check()
     return out
 
 

@@ -21,8 +21,6 @@ constexpr int MAXSEG = 32;  // segments per multi-segment launch (kernel-paramet
 // kernels launched by this library (all entry points, all streams): lets a
 // benchmark count exactly which launches it timed
 unsigned long long g_launches = 0;
-unsigned long long* g_dbg = nullptr;  // experiments: per-warp timestamps
-int g_dbg_flags = 0;                 // experiments: bit 0 = skip the gather kernel, bit 1 = empty gather
 inline void count_launch(unsigned k = 1) { __atomic_fetch_add(&g_launches, (unsigned long long)k, __ATOMIC_RELAXED); }
 
 inline uint64_t nblocks(uint64_t n) { return (n + BLOCK - 1) / BLOCK; }
@@ -71,19 +69,33 @@ SidecarView sidecar_view(const void* sc, uint64_t n) {
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
-// Persistent grid: as many CTAs as fit on the device at once, capped by the
-// number of tiles (each warp takes tiles in ticket order).
+// Launch geometry is cached per device ordinal: the dynamic shared-memory
+// opt-in (cudaFuncSetAttribute) is per device context, and devices may differ
+// in SM count.  Zero-initialised caches hold value + 1 (0 = not yet computed).
+constexpr int MAXDEV = 64;
+inline int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d >= 0 && d < MAXDEV) ? d : 0;
+}
+inline int dev_sms(int dev) {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return sms > 0 ? sms : 1;
+}
+
+// Persistent grid: as many CTAs as fit on the device at once (per device),
+// after opting the kernel into `smem` bytes of dynamic shared memory there.
 template <typename K>
-int grid_cap(K kernel, size_t smem, int& cache) {
-  if (cache < 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, CTA_THREADS, smem);
-    cache = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
+int grid_cap(K kernel, int threads, size_t smem, int (&cache)[MAXDEV]) {
+  const int dev = cur_dev();
+  if (cache[dev] == 0) {
+    int occ = 0;
+    if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
+    cache[dev] = (occ > 0 ? occ : 1) * dev_sms(dev) + 1;
   }
-  return cache;
+  return cache[dev] - 1;
 }
 
 struct WsView {
@@ -113,15 +125,8 @@ template <int SRC, int NSEG, bool FAST>
 int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   constexpr int NW = enc_warps(SRC);
   const size_t smem = (size_t)NW * (SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4);
-  static int cap = -1;
-  if (cap < 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(k_tile_encode<SRC, NSEG, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tile_encode<SRC, NSEG, FAST>, 32 * NW, smem);
-    cap = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
-  }
+  static int caps[MAXDEV];
+  const int cap = grid_cap(k_tile_encode<SRC, NSEG, FAST>, 32 * NW, smem, caps);
   // one CTA per tile up to one per SM: a small message is spread over as many
   // SMs as it has tiles (a tile's encode is a latency chain of ~1100
   // instructions; 24 tiles on one SM would serialise on its issue slots)
@@ -161,18 +166,11 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   int rc = (int)cudaGetLastError();
   if (rc) return rc;
-  if (g_dbg_flags & 1) return 0;
   if (a.slotted_out) return 0;  // slotted output: the consumer reads the slots
   count_launch();
   // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
-  static int gcap = -1;
-  if (gcap < 0) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_gather<NSEG>, GATHER_THREADS, 0);
-    gcap = (occ > 0 ? occ : 1) * (sms > 0 ? sms : 1);
-  }
+  static int gcaps[MAXDEV];
+  const int gcap = grid_cap(k_gather<NSEG>, GATHER_THREADS, 0, gcaps);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)std::min<uint64_t>((gbase + GATHER_THREADS / 32 - 1) / (GATHER_THREADS / 32),
                                                   (uint64_t)gcap));
@@ -205,6 +203,34 @@ __global__ void k_copy_blob(const uint4* __restrict__ src, uint4* __restrict__ d
   const uint64_t nch = (len + 15) >> 4;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nch; i += (uint64_t)gridDim.x * blockDim.x)
     dst[i] = __ldcs(src + i);
+}
+
+// dst = src (f32) with the first non-finite src offset (+ report_base)
+// recorded like codec.py:79-86: the verbatim-kept parts of a collective's
+// input (the scatter root's own block, a single rank's buffer) are checked
+// the same way the encoder checks everything it compresses.
+__global__ void k_copy_checked(const float4* __restrict__ src, float4* __restrict__ dst, uint64_t n, Status* st,
+                               uint64_t report_base) {
+  const uint64_t n4 = n >> 2, stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  for (uint64_t i = t0; i < n4; i += stride) {
+    const float4 v = __ldcs(src + i);
+    __stcs(dst + i, v);
+    if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) {
+      const float f[4] = {v.x, v.y, v.z, v.w};
+      for (int k = 0; k < 4; ++k)
+        if (!isfinite(f[k])) {
+          atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + 4 * i + k));
+          break;
+        }
+    }
+  }
+  if (t0 < (n & 3)) {
+    const uint64_t i = 4 * n4 + t0;
+    const float v = reinterpret_cast<const float*>(src)[i];
+    reinterpret_cast<float*>(dst)[i] = v;
+    if (!isfinite(v)) atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + i));
+  }
 }
 
 struct CopyItems {
@@ -279,20 +305,14 @@ PFN_batchMemOp p_batch() {
 
 }  // namespace
 
-// experiments only: per-warp timestamps of the next compress launch
 
 namespace {
 template <int NSEG>
 int launch_decode(DecodeMultiArgs<NSEG>& a, cudaStream_t s, int reserve_sms = 0) {
   const size_t smem = (size_t)WARPS * dec_warp_smem(NSEG);  // per warp: value tile + stagings
-  static int cap = -1, per_sm = 1;
-  if (cap < 0) {
-    grid_cap(k_tile_decode<NSEG>, smem, cap);
-    int dev = 0, sms = 1;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    per_sm = std::max(1, cap / std::max(1, sms));
-  }
+  static int caps[MAXDEV];
+  const int cap = grid_cap(k_tile_decode<NSEG>, CTA_THREADS, smem, caps);
+  const int per_sm = std::max(1, cap / dev_sms(cur_dev()));
   // leave `reserve_sms` SMs free (a concurrent NVLink copy)
   const int lim = std::max(per_sm, cap - reserve_sms * per_sm);
   const uint64_t want = (a.total_tiles + WARPS - 1) / WARPS;
@@ -321,19 +341,10 @@ int decode_one(const uint8_t* blob, const void* sidecar, const float* local, int
 
 extern "C" {
 
-int gz_debug_set_timestamps(void* p) {
-  g_dbg = reinterpret_cast<unsigned long long*>(p);
-  return 0;
-}
 // profiling only: write the GPU's %globaltimer (ns) into *dst, stream-ordered
 int gz_debug_stamp(void* dst, gz_stream_t stream) {
   k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(dst));
   return (int)cudaGetLastError();
-}
-// experiments only: bit 0 = skip the gather kernel (output incomplete)
-int gz_debug_set_flags(int f) {
-  g_dbg_flags = f;
-  return 0;
 }
 
 uint64_t gz_compress_bound(uint64_t n) { return HEADER_BYTES + nblocks(n) * MAX_BLOCK_BYTES + 64; }
@@ -366,12 +377,10 @@ int gz_compress(const float* x, uint64_t n, double eb, uint32_t block, uint8_t* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView sv = sidecar_view(sidecar, n);
-  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.widths, 0, 0, 0, 0};
+  a.seg[0] = Seg{x, n, blob, d_len, sv.tile_off, sv.widths, 0, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   a.blk_off = d_block_offsets;
-  a.dbg = g_dbg;
-  a.dbg_flags = g_dbg_flags;
   const WsView wv = carve(ws, ntiles_of(n));
   a.ws = wv.hdr;
   a.tile_rel = wv.tile_rel;
@@ -474,12 +483,13 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
   count_launch(4);  // idx_segments, idx_chunks, idx_resolve, idx_emit
   idx_segments<<<(unsigned)nseg, 160, 0, s>>>(payload, payload_len, iw);
   const size_t csm = (size_t)CH * NE * 4;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[MAXDEV];
+  const int dev = cur_dev();
+  if (!attr[dev]) {  // the opt-in is per device context
     cudaFuncSetAttribute(idx_chunks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csm);
     cudaFuncSetAttribute(idx_emit, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)EMIT_SMEM);
     cudaFuncSetAttribute(idx_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RESOLVE_SMEM_MAX);
-    attr = true;
+    attr[dev] = true;
   }
   idx_chunks<<<(unsigned)nch, 160, csm, s>>>(nseg, iw);
   {
@@ -488,7 +498,14 @@ int gz_index(const uint8_t* blob, uint64_t payload_len, uint64_t n, void* sideca
     idx_resolve<<<1, staged ? 512 : 32, staged ? rsm : 0, s>>>(nch, iw, staged);
   }
   idx_emit<<<(unsigned)((nseg + EG - 1) / EG), CH, EMIT_SMEM, s>>>(payload, payload_len, nseg, n, iw, st);
-  if (nblocks(n) > payload_len / 5 + 1) return (int)cudaGetLastError();  // certainly truncated: no sidecar
+  if (nblocks(n) > payload_len / 5 + 1) {
+    // certainly truncated (a block has at least 5 bytes): idx_emit reports the
+    // first failing block of the walk; this bound makes the failure explicit
+    // even if the walk stopped early, and no sidecar is built
+    count_launch();
+    k_record_error<<<1, 1, 0, s>>>(st, (unsigned long long)(((payload_len / 5) << 24) | DE_TRUNC));
+    return (int)cudaGetLastError();
+  }
   const uint64_t nt = ntiles_of(n);
   const uint64_t work = nt + 1;
   SidecarView sv = sidecar_view(sidecar, n);
@@ -509,7 +526,7 @@ int gz_reduce_step(const uint8_t* blob_in, const void* sidecar_in, const float* 
   EncodeArgs<1> a;
   std::memset(&a, 0, sizeof(a));
   SidecarView so = sidecar_view(sidecar_out, m);
-  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
+  a.seg[0] = Seg{local, m, blob_out, d_len_out, so.tile_off, so.widths, 0, 0, 0, 0, 0};
   a.nseg = 1;
   a.qp = make_qparams(eb);
   const WsView wv = carve(ws, ntiles_of(m));
@@ -553,7 +570,7 @@ int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int
   a.tile_rel = wv.tile_rel;
   a.scratch = wv.scratch;
   if (slotted) {
-    a.seg[0] = Seg{local, m, nullptr, nullptr, nullptr, io->out_widths, 0, 0, 0, 0};
+    a.seg[0] = Seg{local, m, nullptr, nullptr, nullptr, io->out_widths, 0, 0, 0, 0, io->report_base};
     a.tile_rel = io->out_sizes;
     a.scratch = io->out_slots;
     a.slotted_out = 1;  // the encoder's last CTA re-zeroes the claim counter (no gather)
@@ -562,7 +579,7 @@ int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int
   } else {
     if (io->post_flag || io->wait_flag) return GZ_EINVAL;
     SidecarView so = sidecar_view(io->sidecar_out, m);
-    a.seg[0] = Seg{local, m, io->blob_out, io->d_len_out, so.tile_off, so.widths, 0, 0, 0, 0};
+    a.seg[0] = Seg{local, m, io->blob_out, io->d_len_out, so.tile_off, so.widths, 0, 0, 0, 0, io->report_base};
   }
   a.nseg = 1;
   a.qp = make_qparams(eb);
@@ -602,13 +619,14 @@ int gz_step_reduce(const gz_step_io* io, const float* local, uint64_t m, double 
   a.local = local;
   a.op = op;
   a.st = reinterpret_cast<Status*>(d_status);
+  a.report_base = io->report_base;
   return launch_decode<1>(a, (cudaStream_t)stream);
 }
 
 int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg, double eb, uint8_t* payload,
                          const uint64_t* h_seg_blob_off, uint64_t* d_seg_len, void* sidecars,
-                         const uint64_t* h_seg_sidecar_off, void* ws, uint64_t ws_bytes, gz_status* d_status,
-                         gz_stream_t stream) {
+                         const uint64_t* h_seg_sidecar_off, const uint64_t* h_seg_report_off, void* ws,
+                         uint64_t ws_bytes, gz_status* d_status, gz_stream_t stream) {
   if (!check_eb(eb)) return GZ_EBOUND;
   if (!h_counts || !payload || !h_seg_blob_off || !d_seg_len || !ws || !d_status) return GZ_EINVAL;
   uint64_t total = 0, tiles_all = 0;
@@ -632,7 +650,8 @@ int gz_compress_segments(const float* x, const uint64_t* h_counts, uint32_t nseg
       const uint64_t n = h_counts[i];
       SidecarView sv{nullptr, nullptr};
       if (sidecars) sv = sidecar_view(reinterpret_cast<uint8_t*>(sidecars) + h_seg_sidecar_off[i], n);
-      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.widths, 0, 0, 0, tiles};
+      a.seg[j] = Seg{x + xoff, n, payload + h_seg_blob_off[i], d_seg_len + i, sv.tile_off, sv.widths, 0, 0, 0, tiles,
+                     h_seg_report_off ? h_seg_report_off[i] : xoff};
       tiles += ntiles_of(n);
       xoff += n;
     }
@@ -742,6 +761,19 @@ int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64
   return (int)cudaGetLastError();
 }
 
+int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_base, gz_status* d_status,
+                    gz_stream_t stream) {
+  if (n == 0) return 0;
+  if (!src || !dst || !d_status || !aligned16(src) || !aligned16(dst)) return GZ_EINVAL;
+  const uint64_t want = ((n >> 2) + 255) / 256;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * dev_sms(cur_dev())));
+  count_launch();
+  k_copy_checked<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(src),
+                                                          reinterpret_cast<float4*>(dst), n,
+                                                          reinterpret_cast<Status*>(d_status), report_base);
+  return (int)cudaGetLastError();
+}
+
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream) {
   return gz_copy_items_sms(items, count, 0, stream);
 }
@@ -768,22 +800,24 @@ int gz_copy_items_sms(const gz_copy_item* items, uint32_t count, int sms_budget,
 // ---- fixed-rate baseline codec (codec.py:442-489) -------------------------
 uint64_t gz_fr_bound(uint64_t n, uint32_t bits) { return FR_HEADER_BYTES + (n * (uint64_t)bits + 7) / 8 + 16; }
 
+uint64_t gz_fr_workspace_bytes(void) { return (sizeof(FrScratch) + 15) & ~15ull; }
+
 int gz_fr_compress(const float* x, uint64_t n, uint32_t bits, uint8_t* out, uint64_t out_cap, uint64_t* d_len,
-                   void* ws8, gz_status* d_status, gz_stream_t stream) {
+                   void* ws, gz_status* d_status, gz_stream_t stream) {
   if (bits < 1 || bits > 16) return GZ_EINVAL;
-  if ((!x && n) || !out || !d_len || !ws8 || !d_status) return GZ_EINVAL;
+  if ((!x && n) || !out || !d_len || !ws || !d_status) return GZ_EINVAL;
   if (out_cap < FR_HEADER_BYTES + (n * (uint64_t)bits + 7) / 8) return GZ_ECAPACITY;
   cudaStream_t s = (cudaStream_t)stream;
-  int* mm = reinterpret_cast<int*>(ws8);
-  const int init[2] = {0x7FFFFFFF, (int)0x80000000};
-  cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, s);
+  FrScratch* sc = reinterpret_cast<FrScratch*>(ws);
   const uint64_t groups = (n + 31) / 32;
   if (n) {
-    count_launch();
-    k_fr_minmax<<<592, 256, 0, s>>>(x, n, mm, reinterpret_cast<Status*>(d_status));
+    count_launch(3);
+    k_fr_init<<<1, 32, 0, s>>>(sc);
+    k_fr_minmax<<<592, 256, 0, s>>>(x, n, sc, reinterpret_cast<Status*>(d_status));
+    k_fr_zero_lanes<<<592, 256, 0, s>>>(x, n, sc);
   }
   count_launch();
-  k_fr_encode<<<(unsigned)std::max<uint64_t>(1, (groups + 255) / 256), 256, 0, s>>>(x, n, (int)bits, mm, out, d_len);
+  k_fr_encode<<<(unsigned)std::max<uint64_t>(1, (groups + 255) / 256), 256, 0, s>>>(x, n, (int)bits, sc, out, d_len);
   return (int)cudaGetLastError();
 }
 

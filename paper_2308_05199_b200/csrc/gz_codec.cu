@@ -28,6 +28,7 @@ struct Seg {
   uint64_t gcta_base;      // first gather group of this segment
   uint64_t gcta_n;         // gather groups of this segment
   uint64_t tile_base;      // first slot of this segment in tile_rel / scratch
+  uint64_t report_base;    // offset of x[0] in the caller's buffer (first_nonfinite reports)
 };
 
 template <int NSEG>
@@ -41,8 +42,6 @@ struct EncodeArgs {
   QParams qp;
   uint64_t* blk_off;       // optional per-block payload offsets (segment 0 only)
   TileWs* ws;
-  unsigned long long* dbg; // optional per-warp timestamps (experiments)
-  int dbg_flags;           // experiments: bit 1 = gather kernel skips its work, bits 4-6 = global claim share
   uint32_t* tile_rel;      // per tile: compressed size (phase A -> phase B)
   uint8_t* scratch;        // per tile one TILE_SLOT-byte slot (16-byte aligned)
   Status* st;
@@ -105,17 +104,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 // Wait (thread 0) until *flag >= 1, written by a peer GPU; a release/acquire
 // pair with the producer's __threadfence_system + store.  Bounded: a flag
-// that never arrives traps after ~20 s instead of hanging the GPU.
-__device__ __forceinline__ void wait_flag_sys(const unsigned int* flag) {
+// that never arrives makes the wait give up after GZ_FLAG_TIMEOUT_NS and
+// report it (the caller skips its work and records comm_error) instead of
+// hanging the GPU.
+constexpr unsigned long long FLAG_TIMEOUT_NS = 20000000000ull;
+__device__ __forceinline__ bool wait_flag_sys(const unsigned int* flag) {
   unsigned int v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-  if (v >= 1u) return;
+  if (v >= 1u) return true;
   const unsigned long long t0 = gtimer();
   do {
     __nanosleep(64);
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flag) : "memory");
-    if (gtimer() - t0 > 20000000000ull) __trap();
+    if (gtimer() - t0 > FLAG_TIMEOUT_NS) return false;
   } while (v < 1u);
+  return true;
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
@@ -141,13 +144,22 @@ __device__ __forceinline__ float np_maximum_f(float a, float b) {  // collective
   return isnan(a) ? a : (a > b ? a : b);
 }
 
-// dst = op(local, decoded) (collectives.py:32-39, local first), coalesced
+// dst = op(local, decoded) (collectives.py:32-39, local first), coalesced.
+// A non-finite local value is reported like the encoder does (the last step
+// of a standalone reduce-scatter is the only place that reads its chunk).
 __device__ __forceinline__ void drain_values_op(const float* xs, const float* __restrict__ local, int op,
-                                                float* __restrict__ dst, uint64_t v0, int nval, int lane) {
+                                                float* __restrict__ dst, uint64_t v0, int nval, int lane,
+                                                Status* st, uint64_t report_base) {
+  bool bad = false;
   for (int i = lane; i < nval; i += 32) {
     const int row = i >> 5, col = i & 31;
     const float d = xs[xs_index(row, col >> 2) + (col & 3)], l = __ldcs(local + v0 + i);
+    bad |= !isfinite(l);
     __stcs(dst + v0 + i, op == 0 ? __fadd_rn(l, d) : np_maximum_f(l, d));
+  }
+  if (__any_sync(0xFFFFFFFFu, bad)) {
+    for (int i = lane; i < nval; i += 32)
+      if (!isfinite(local[v0 + i])) atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + v0 + i));
   }
 }
 
@@ -437,10 +449,12 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
       uint32_t zl[32];
       zor = slow_block(row, cnt, a.qp, zl, &flags);
       store_codes(zs, lane, x0, zl);
-      if (flags & 4) {  // codec.py:83-85: report the first non-finite offset
+      if (flags & 4) {  // codec.py:83-85: report the first non-finite offset of the caller's buffer
+        // (in the fused step the values are op(local, received): only `local` is this rank's input)
+        const float* src = S.x + v0 + (uint64_t)lane * 32;
         for (int j = 0; j < cnt; ++j)
-          if (!isfinite(row[j])) {
-            atomicMin(&a.st->first_nonfinite, (unsigned long long)(v0 + (uint64_t)lane * 32 + j));
+          if (!isfinite(SRC == SRC_STEP ? src[j] : row[j])) {
+            atomicMin(&a.st->first_nonfinite, (unsigned long long)(S.report_base + v0 + (uint64_t)lane * 32 + j));
             break;
           }
       }
@@ -551,6 +565,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
   __shared__ unsigned int s_next;
+  __shared__ int s_abort;
   // the gather kernel may be scheduled as soon as SMs free up; it waits for
   // this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
@@ -564,12 +579,18 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   if (SRC == SRC_STEP) init_step_table(s_step, a.in_tw);
   if (tid == 0) {
     s_next = 0;
-    if (a.wait_flag) wait_flag_sys(a.wait_flag);  // the ring's "input ready" (or "slots free") flag
+    s_abort = 0;
+    // the ring's "input ready" (or "slots free") flag; a flag that never
+    // arrives is reported and the CTA skips its tiles (the step's completion
+    // is still posted below, so the peers' streams drain)
+    if (a.wait_flag && !wait_flag_sys(a.wait_flag)) {
+      atomicMin(&a.st->comm_error, (unsigned long long)COMM_FLAG_TIMEOUT);
+      s_abort = 1;
+    }
   }
   __syncthreads();
   const uint64_t c = blockIdx.x;
   const uint64_t pol_in = pol_evict_first(), pol_keep = pol_evict_last();
-  const unsigned long long ts0 = a.dbg ? gtimer() : 0;
 
   // ---- tile claiming (over all segments): most tiles are split into
   // contiguous per-CTA ranges claimed through a shared-memory counter (warps
@@ -579,8 +600,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   const unsigned int total = (unsigned int)a.total_tiles;
   // global share 1/2^tshift: 1/32 for plain compression (2^24: 52 -> 48 us
   // vs 1/8, tools/exp/tail.py; no change at 2^27), 1/8 for the fused step
-  const unsigned tdef = SRC == SRC_PLAIN ? 5u : 3u;
-  const unsigned tshift = ((a.dbg_flags >> 4) & 7) ? ((a.dbg_flags >> 4) & 7) : tdef;  // experiments: bits 4-6
+  const unsigned tshift = SRC == SRC_PLAIN ? 5u : 3u;
   const unsigned int stat = total - (total >> tshift);
   const unsigned int r0 = (unsigned int)(((uint64_t)stat * c) / gridDim.x);
   const unsigned int nr = (unsigned int)(((uint64_t)stat * (c + 1)) / gridDim.x) - r0;
@@ -613,18 +633,18 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
         m.ts = a.in_tile_off[jn];
         m.te = a.in_tile_off[jn + 1];
       }
+      if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;  // corrupt sidecar
       m.w = a.in_w[(uint64_t)jn * TB + lane];
     }
     return m;
   };
   const uint8_t* const in_base = a.in_slots ? a.in_slots : a.in_blob + HEADER_BYTES;
-  unsigned int j = claim();
+  unsigned int j = s_abort ? total : claim();
   unsigned int j1 = j < total ? claim() : total;
   InTile in_cur{0, 0, 0};
   InMeta m_cur = ONEBUF ? load_meta(j) : InMeta{0, 0, 0};
   if (j < total && !ONEBUF) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
-  unsigned long long wait_ns = 0, ndone = 0;
   uint32_t dummy = 0;
   while (j < total) {
     InMeta m_nxt{0, 0, 0};
@@ -658,7 +678,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
         atomicAdd(&a.ws->agg3[g >> 10], (unsigned)tb);
       }
     }
-    ++ndone;
     __syncwarp();
     buf ^= 1;
     j = j1;
@@ -684,12 +703,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
         }
       }
     }
-  }
-  if (a.dbg && lane == 0) {  // experiments: per-warp timestamps
-    unsigned long long* d = a.dbg + (c * NW + warp) * 12;
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    d[0] = ts0; d[1] = gtimer(); d[2] = ndone; d[3] = wait_ns; d[4] = c; d[5] = smid;
   }
 }
 
@@ -755,7 +768,7 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
   const int tid = threadIdx.x, lane = tid & 31;
   TileWs* ws = a.ws;
   const uint64_t nwarps = (uint64_t)gridDim.x * (GATHER_THREADS / 32);
-  const uint64_t cend = (a.dbg_flags & 2) ? 0 : a.ngctas;
+  const uint64_t cend = a.ngctas;
   for (uint64_t c = (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (tid >> 5); c < cend; c += nwarps) {
     int k = 0;
     if (NSEG > 1) {
@@ -902,6 +915,7 @@ struct DecodeMultiArgs {
   const float* local;      // NSEG == 1 only: y = op(local, decoded)
   int op;
   Status* st;
+  uint64_t report_base;    // offset of local[0] in the caller's buffer (first_nonfinite reports)
 };
 
 // Stages per warp: 2 (one tile ahead) for local blobs; 3 (two tiles ahead)
@@ -946,6 +960,9 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
         m.ts = S.tile_off[lt];
         m.te = S.tile_off[lt + 1];
       }
+      // a corrupt sidecar must not overflow the staging buffer: stage nothing,
+      // block_start() then reports the mismatch
+      if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;
     }
     return m;
   };
@@ -996,7 +1013,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     const int start = block_start(stage_t, bq[0], (int)(md[0].te - md[0].ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
     decode_row<0>(stage_t, bq[0], start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
-    if (NSEG == 1 && a.local) drain_values_op(xs, a.local, a.op, S.y, v0, nval, lane);
+    if (NSEG == 1 && a.local) drain_values_op(xs, a.local, a.op, S.y, v0, nval, lane, a.st, a.report_base);
     else drain_values(xs, S.y, v0, nval, lane);
     __syncwarp();
 #pragma unroll

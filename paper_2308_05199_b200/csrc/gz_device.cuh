@@ -69,8 +69,10 @@ struct TileWs {
 struct Status {                          // error reporting (host-reset to ~0)
   unsigned long long first_nonfinite;    // codec.py:83-85
   unsigned long long decode_error;       // (block << 24) | (width << 8) | code, min over blocks
-  unsigned long long pad[2];
+  unsigned long long trailing;           // trailing byte count of a DE_TRAIL error (codec.py:321-322)
+  unsigned long long comm_error;         // COMM_* code of a peer-flag wait that gave up (~0 if none)
 };
+enum CommErr : unsigned { COMM_FLAG_TIMEOUT = 1 };
 enum DecodeErr : unsigned { DE_WIDTH = 1, DE_TRUNC = 2, DE_TRAIL = 3, DE_SIDECAR = 4, DE_HEADER = 5 };
 
 struct QParams {

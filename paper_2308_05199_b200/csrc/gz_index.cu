@@ -250,13 +250,14 @@ __global__ void __launch_bounds__(CH) idx_emit(const uint8_t* payload, uint64_t 
     }
     if (blk == nb - 1 && pos != psize) {  // 321-322
       idx_error(st, nb, 0, DE_TRAIL);
-      st->pad[0] = psize - pos;
+      st->trailing = psize - pos;
       return;
     }
     ++blk;
   }
-  // the chain ran out of payload inside this segment before nb blocks
-  if (blk < nb && pos >= psize && pos < send) idx_error(st, blk, 0, DE_TRUNC);
+  // the chain ran out of payload before nb blocks (also when the payload
+  // ends exactly on this segment's boundary: pos == psize == send)
+  if (blk < nb && pos >= psize) idx_error(st, blk, 0, DE_TRUNC);
 }
 
 __global__ void idx_sidecar(const IndexWs ws, uint64_t n, uint64_t psize, uint64_t* tile_off) {

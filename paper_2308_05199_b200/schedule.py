@@ -89,3 +89,68 @@ def scatter_route(N: int, root: int = 0):
         parent = None if vr == 0 else order[vr - extent]
         routes[order[vr]] = (parent, vr, [(order[c], lo, hi) for c, lo, hi in sends])
     return routes
+
+
+# ---------------------------------------------------------------------------
+# recursive doubling (collectives.py:349-424, RecursiveDoublingPlan 48-86)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class RdSend:
+    """Send message number `k` to `dst`.  src is None: the message is
+    compress(data).  Otherwise first data = op(data, decompress(src's message
+    k_in)) and the message is compress(data) -- one fused kernel."""
+
+    k: int
+    dst: int
+    src: int | None = None
+    k_in: int | None = None
+
+
+@dataclass(frozen=True)
+class RdRecvLast:
+    """data = op(data, decompress(src's message k_in)) (reduce) or
+    data = decompress(...) (a donor receiving its absorber's result)."""
+
+    src: int
+    k_in: int
+    reduce: bool
+
+
+def rd_allreduce_plan(N: int, i: int) -> list:
+    """rd_allreduce_c for rank i of N, in fused form.  Message numbers: 0 = a
+    donor's buffer, 1..steps = the exchange steps, steps+1 = an absorber's
+    final result sent back to its donor (collectives.py:381-435)."""
+    if N == 1:
+        return []
+    pof2 = 1 << (N.bit_length() - 1)
+    r = N - pof2
+    steps = pof2.bit_length() - 1
+    K = steps + 2
+
+    def role(j):
+        return ("donor" if j % 2 == 0 else "absorber") if j < 2 * r else "direct"
+
+    def remapped(j):
+        return j // 2 if role(j) == "absorber" else j - r
+
+    def actual(v):
+        return 2 * v + 1 if v < r else v + r
+
+    if role(i) == "donor":  # 381-386, 430-435
+        return [RdSend(k=0, dst=i + 1), RdRecvLast(src=i + 1, k_in=K - 1, reduce=False)]
+    part = [actual(remapped(i) ^ (1 << t)) for t in range(steps)]
+    plan = []
+    if role(i) == "absorber":  # 389-397: the donor folded in, fused with the step-0 compression
+        plan.append(RdSend(k=1, dst=part[0], src=i - 1, k_in=0))
+    else:
+        plan.append(RdSend(k=1, dst=part[0]))
+    for t in range(steps):  # 399-418
+        if t + 1 < steps:
+            plan.append(RdSend(k=t + 2, dst=part[t + 1], src=part[t], k_in=t + 1))
+        elif role(i) == "absorber":  # 420-427: the result goes back to the donor
+            plan.append(RdSend(k=K - 1, dst=i - 1, src=part[t], k_in=t + 1))
+        else:
+            plan.append(RdRecvLast(src=part[t], k_in=t + 1, reduce=True))
+    return plan

@@ -81,7 +81,7 @@ def compress_segments(x: torch.Tensor, counts, eb: float, ws: Workspace, stream=
     if check:
         ws.reset_status(stream)
     L.check(lib.gz_compress_segments(x.data_ptr(), h_counts, nseg, float(eb), payload.data_ptr(), h_slot,
-                                     d_lens.data_ptr(), sidecars.data_ptr(), h_sc, tws.data_ptr(), tws.numel(),
+                                     d_lens.data_ptr(), sidecars.data_ptr(), h_sc, None, tws.data_ptr(), tws.numel(),
                                      ws.status_ptr(), _stream(stream)), "gz_compress_segments")
     if check:
         st = ws.read_status(stream)

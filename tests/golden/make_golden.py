@@ -280,6 +280,43 @@ def fixed_rate_cases(codec):
     return len(cfgs)
 
 
+def fixed_rate_zero_cases(codec):
+    """Fixed-rate blobs whose min and/or max is a zero: the header carries the
+    sign numpy's SIMD reduction returns (order-dependent for +-0).  Generated on
+    an AVX-512 host (numpy dispatch AVX512_SKX); other hosts' numpy may differ,
+    which is why the oracle restates the AVX-512 reduction explicitly."""
+    from numpy._core._multiarray_umath import __cpu_features__ as feats
+
+    assert feats.get("AVX512_SKX"), "generate these on an AVX-512 host"
+    rng = np.random.default_rng(4242)
+    datas, blobs, ys, bits = [], [], [], []
+    lengths = [1, 2, 3, 16, 17, 18, 31, 33, 64, 129, 130, 257, 1000, 4097, 20001]
+    for k, n in enumerate(lengths * 2):
+        x = np.zeros(n, np.float32)
+        kind = k % 4
+        if kind == 1:
+            x = rng.integers(0, 3, n).astype(np.float32)     # min is a zero
+        elif kind == 2:
+            x = -rng.integers(0, 3, n).astype(np.float32)    # max is a zero
+        elif kind == 3:
+            x = rng.uniform(-1, 1, n).astype(np.float32)
+            x[rng.random(n) < 0.3] = 0.0                    # zeros inside, extremum not zero
+        z = x == 0
+        x[z] = np.where(rng.random(int(z.sum())) < rng.random(), -0.0, 0.0).astype(np.float32)
+        b = int(1 + k % 16)
+        blob = codec.fixed_rate_compress(x, b)
+        datas.append(x)
+        blobs.append(np.frombuffer(blob, np.uint8).copy())
+        ys.append(codec.fixed_rate_decompress(blob))
+        bits.append(b)
+    out = {"bits": np.array(bits, np.int64), "count": np.array(len(bits))}
+    pack_list("x", datas, out)
+    pack_list("blob", blobs, out)
+    pack_list("y", ys, out)
+    np.savez_compressed(os.path.join(HERE, "fixed_rate_zero_cases.npz"), **out)
+    return len(bits)
+
+
 def digests(codec):
     x = smooth(1 << 24)
     d = {"cfg1_input_sha256": hashlib.sha256(x.tobytes()).hexdigest()}
@@ -301,5 +338,6 @@ if __name__ == "__main__":
     print("codec cases:", codec_cases(codec))
     print("ring cases:", len(ring_cases(codec, collectives, simnet)))
     print("fixed-rate cases:", fixed_rate_cases(codec))
+    print("fixed-rate signed-zero cases:", fixed_rate_zero_cases(codec))
     print("scatter cases:", scatter_cases(codec, collectives, simnet))
     print("digests:", digests(codec))

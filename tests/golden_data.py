@@ -111,3 +111,10 @@ def fixed_rate_cases():
     z = np.load(os.path.join(GOLDEN_DIR, "fixed_rate_cases.npz"))
     xs, blobs, ys = _unpack(z, "x"), _unpack(z, "blob"), _unpack(z, "y")
     return [(xs[k], int(z["bits"][k]), blobs[k].tobytes(), ys[k]) for k in range(int(z["count"]))]
+
+
+def fixed_rate_zero_cases():
+    """Fixed-rate blobs whose min / max is a signed zero (numpy's AVX-512 choice)."""
+    z = np.load(os.path.join(GOLDEN_DIR, "fixed_rate_zero_cases.npz"))
+    xs, blobs, ys = _unpack(z, "x"), _unpack(z, "blob"), _unpack(z, "y")
+    return [(xs[k], int(z["bits"][k]), blobs[k].tobytes(), ys[k]) for k in range(int(z["count"]))]

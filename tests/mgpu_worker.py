@@ -172,6 +172,62 @@ def main():
         if "sum" not in str(err):
             failures.append(f"bad counts message {err}")
     checked += 1
+    # a captured ring graph must survive other collectives growing the communicator's
+    # workspace (the ring has its own, sized once per setup)
+    n = 1 << 20
+    bufs = [O.smooth_field(n, 0.13 * r) for r in range(world)]
+    expect = O.ring_allreduce(bufs, 1e-4, "sum")[rank].tobytes()
+    x = torch.from_numpy(bufs[rank]).to(dev)
+    out = torch.empty_like(x)
+    for rep in range(3):
+        c.ring_allreduce(x, 1e-4, "sum", out=out)
+    big = [O.smooth_field(6_000_000, 0.3 * r) for r in range(world)]
+    c.rd_allreduce(torch.from_numpy(big[rank]).to(dev), 1e-4)  # grows the shared tile workspace
+    if rank == 0:
+        xb = torch.from_numpy(O.smooth_field(8_000_000, 0.2)).to(dev)
+    c.binomial_scatter(xb if rank == 0 else None, 1e-4, root=0)
+    for rep in range(2):
+        c.ring_allreduce(x, 1e-4, "sum", out=out)  # graph replay
+        torch.cuda.synchronize()
+        if out.cpu().numpy().tobytes() != expect:
+            failures.append(f"ring graph replay after workspace growth rep={rep}")
+        checked += 1
+    # errors (codec.py:79-86 via collectives.py:202-205): a non-finite input value raises on
+    # EVERY rank with the offset of the first bad value in rank order; the communicator
+    # stays usable afterwards
+    def expect_error(what, fn, frag):
+        nonlocal checked
+        try:
+            fn()
+            failures.append(f"{what}: no error raised")
+        except ValueError as err:
+            if frag not in str(err):
+                failures.append(f"{what}: message {err!r}, expected {frag!r}")
+        checked += 1
+    n = 100_003
+    for bad_rank, off in ((1, 54_321), (world - 1, 7)):
+        for kind in ("allreduce", "reduce_scatter", "rd"):
+            xs = [O.smooth_field(n, 0.5 * r) for r in range(world)]
+            xs[bad_rank][off] = np.nan
+            if world > 2 and bad_rank == 1:
+                xs[2][3] = np.inf  # later in rank order: the rank-1 offset is reported
+            xt = torch.from_numpy(xs[rank]).to(dev)
+            fn = {"allreduce": lambda: c.ring_allreduce(xt, 1e-4),
+                  "reduce_scatter": lambda: c.ring_reduce_scatter(xt, 1e-4),
+                  "rd": lambda: c.rd_allreduce(xt, 1e-4)}[kind]
+            expect_error(f"{kind} nan rank={bad_rank} off={off}", fn, f"non-finite value at offset {off}")
+    for root, off in ((0, 3), (0, n - 1), (world - 1, 3), (world - 1, n - 1)):  # own block / a sent block
+        data = O.smooth_field(n, 0.9)
+        data[off] = -np.inf
+        xt = torch.from_numpy(data).to(dev) if rank == root else None
+        expect_error(f"scatter inf root={root} off={off}", lambda: c.binomial_scatter(xt, 1e-4, root=root),
+                     f"non-finite value at offset {off}")
+    xs = [O.smooth_field(n, 0.5 * r) for r in range(world)]
+    got = c.ring_allreduce(torch.from_numpy(xs[rank]).to(dev), 1e-4)
+    torch.cuda.synchronize()
+    if got.cpu().numpy().tobytes() != O.ring_allreduce(xs, 1e-4)[rank].tobytes():
+        failures.append("allreduce after errors")
+    checked += 1
     flag = torch.tensor([len(failures)], device="cpu" if oversub else dev)
     dist.all_reduce(flag)
     if rank == 0:

@@ -189,6 +189,17 @@ def test_fixed_rate_matches_reference(k, ws):
     assert gz.fixed_rate_decompress(dev, ws).cpu().numpy().tobytes() == y.tobytes()
 
 
+FRZ = G.fixed_rate_zero_cases()
+
+
+@pytest.mark.parametrize("k", range(len(FRZ)))
+def test_fixed_rate_signed_zero_extremum(k, ws):
+    # a zero min / max carries the sign numpy's AVX-512 reduction returns (codec.py:454-455)
+    x, b, blob, y = FRZ[k]
+    assert gz.fixed_rate_compress(x, b, ws) == blob
+    assert gz.fixed_rate_decompress(blob, ws).tobytes() == y.tobytes()
+
+
 def test_fixed_rate_errors(ws):
     with pytest.raises(ValueError, match="bits_per_value"):
         gz.fixed_rate_compress(np.zeros(4, np.float32), 17)
@@ -223,3 +234,22 @@ def test_index_large_reference_blob_and_deep_errors(oracle, ws):
         gz.decompress(ref[:-5], ws)
     with pytest.raises(gz.DecodeError, match="trailing"):
         gz.decompress(ref + b"\x00\x00", ws)
+
+
+@pytest.mark.parametrize("cut_segments", [1, 5, 10, 645])
+def test_truncation_exactly_at_a_segment_boundary(cut_segments, oracle, ws):
+    # all-zero input -> 5-byte blocks; a payload cut at k * 2048 bytes ends on an index
+    # segment boundary with a block ending exactly there: the reference reports the first
+    # missing block (codec.py:307-308), never a silent partial decode (gz_index)
+    n = 32 * 5 * 2048 * (cut_segments + 1) // 5
+    x = np.zeros(n, np.float32)
+    blob = oracle.compress(x, 1e-4)
+    cut = 24 + 2048 * cut_segments
+    nblk = 2048 * cut_segments // 5
+    msg = f"truncated payload at block {nblk}"
+    with pytest.raises(ValueError, match=msg):
+        oracle.decompress(blob[:cut])
+    with pytest.raises(gz.DecodeError, match=msg):
+        gz.decompress(blob[:cut], ws)
+    with pytest.raises(gz.DecodeError, match=msg):
+        gz.decompress(torch.frombuffer(bytearray(blob[:cut]), dtype=torch.uint8).cuda(), ws)

@@ -136,3 +136,34 @@ def test_oracle_fixed_rate_matches_reference(k, oracle):
     x, b, blob, y = FR[k]
     assert oracle.fixed_rate_compress(x, b) == blob
     assert oracle.fixed_rate_decompress(blob).tobytes() == y.tobytes()
+
+
+FRZ = G.fixed_rate_zero_cases()
+
+
+@pytest.mark.parametrize("k", range(len(FRZ)))
+def test_oracle_fixed_rate_signed_zero_extremum(k, oracle):
+    # numpy's x.min()/x.max() pick a zero's sign by SIMD lane order (codec.py:454-455);
+    # the oracle restates the AVX-512 reduction and must reproduce the reference's header
+    x, b, blob, y = FRZ[k]
+    assert oracle.fixed_rate_compress(x, b) == blob
+    assert oracle.fixed_rate_decompress(blob).tobytes() == y.tobytes()
+
+
+def test_avx512_extremum_model_matches_host_numpy(oracle):
+    import math
+
+    from numpy._core._multiarray_umath import __cpu_features__ as feats
+
+    if not feats.get("AVX512_SKX"):
+        pytest.skip("host numpy does not dispatch AVX-512: its signed-zero choice differs by design")
+    rng = np.random.default_rng(11)
+    for t in range(300):
+        n = int(rng.integers(1, 700))
+        x = (rng.integers(0, 2, n) * (1 if t % 2 else -1)).astype(np.float32)
+        z = x == 0
+        x[z] = np.where(rng.random(int(z.sum())) < 0.5, -0.0, 0.0)
+        for op in ("min", "max"):
+            ref = x.min() if op == "min" else x.max()
+            got = oracle.np_extremum_avx512(x, op)
+            assert got == ref and math.copysign(1, got) == math.copysign(1, ref), (n, op)
