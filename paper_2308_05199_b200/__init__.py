@@ -25,10 +25,23 @@ from .codec import (
     fixed_rate_decompress,
     worst_case_blob_bytes,
 )
+from .collectives import CommunicatorSpec, Network, create_network, run_collective
+from .collectives import Counters as OpCounters
+from .metrics import AccuracyStats, CollectiveReport, compression_ratio, max_abs_error, psnr
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "AccuracyStats",
+    "CollectiveReport",
+    "CommunicatorSpec",
+    "Network",
+    "OpCounters",
+    "compression_ratio",
+    "create_network",
+    "max_abs_error",
+    "psnr",
+    "run_collective",
     "BLOCK",
     "HEADER_BYTES",
     "MAGIC",

@@ -215,7 +215,7 @@ __global__ void k_copy_checked(const float4* __restrict__ src, float4* __restric
   const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   for (uint64_t i = t0; i < n4; i += stride) {
     const float4 v = __ldcs(src + i);
-    __stcs(dst + i, v);
+    if (dst) __stcs(dst + i, v);
     if (!(isfinite(v.x) && isfinite(v.y) && isfinite(v.z) && isfinite(v.w))) {
       const float f[4] = {v.x, v.y, v.z, v.w};
       for (int k = 0; k < 4; ++k)
@@ -228,7 +228,7 @@ __global__ void k_copy_checked(const float4* __restrict__ src, float4* __restric
   if (t0 < (n & 3)) {
     const uint64_t i = 4 * n4 + t0;
     const float v = reinterpret_cast<const float*>(src)[i];
-    reinterpret_cast<float*>(dst)[i] = v;
+    if (dst) reinterpret_cast<float*>(dst)[i] = v;
     if (!isfinite(v)) atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + i));
   }
 }
@@ -764,13 +764,35 @@ int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64
 int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_base, gz_status* d_status,
                     gz_stream_t stream) {
   if (n == 0) return 0;
-  if (!src || !dst || !d_status || !aligned16(src) || !aligned16(dst)) return GZ_EINVAL;
+  if (!src || !d_status || !aligned16(src) || (dst && !aligned16(dst))) return GZ_EINVAL;
   const uint64_t want = ((n >> 2) + 255) / 256;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * dev_sms(cur_dev())));
   count_launch();
   k_copy_checked<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<const float4*>(src),
                                                           reinterpret_cast<float4*>(dst), n,
                                                           reinterpret_cast<Status*>(d_status), report_base);
+  return (int)cudaGetLastError();
+}
+
+// out = op(local, recv) elementwise, _apply_op (collectives.py:32-39): "sum"
+// local + recv in binary32 RN, "max" np.maximum(local, recv) (NaN propagates,
+// the second argument wins ties) -- the reduction of the verbatim-payload
+// (lossless / fixed-rate) collectives, whose messages are not fused-decoded.
+__global__ void k_apply_op(const float* a, const float* b, float* out,
+                           uint64_t n, int op) {
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float x = __ldcs(a + i), y = __ldcs(b + i);
+    __stcs(out + i, op == OP_SUM ? __fadd_rn(x, y) : np_maximum(x, y));
+  }
+}
+
+int gz_apply_op(const float* local, const float* recv, float* out, uint64_t n, int op, gz_stream_t stream) {
+  if (n == 0) return 0;
+  if (!local || !recv || !out || (op != OP_SUM && op != OP_MAX)) return GZ_EINVAL;
+  const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n + 255) / 256, 4ull * dev_sms(cur_dev())));
+  count_launch();
+  k_apply_op<<<grid, 256, 0, (cudaStream_t)stream>>>(local, recv, out, n, op);
   return (int)cudaGetLastError();
 }
 

@@ -24,15 +24,20 @@ def ws():
     return gz.Workspace()
 
 
+def _np(o):
+    return o.cpu().numpy() if isinstance(o, torch.Tensor) else np.asarray(o)
+
+
 @pytest.mark.parametrize("case", RING, ids=[f"{c.algo}-N{c.N}-n{c.n}-{c.op}" for c in RING])
 def test_ring_matches_reference(case, ws):
-    outs, rep = C.run_collective(case.algo, case.inputs, eb=case.eb, reduce_op=case.op, record_payloads=True,
-                                 workspace=ws)
+    net = C.create_network(C.CommunicatorSpec(case.N), record_payloads=True)
+    outs, rep = C.run_collective(net, case.algo, case.inputs, eb=case.eb, reduce_op=case.op, workspace=ws)
     assert len(outs) == case.N
     for o, e in zip(outs, case.outputs):
-        assert o.cpu().numpy().tobytes() == e.tobytes()
-    msgs = rep.trace.msgs
-    assert [m[2] for m in msgs] == case.msgs
+        assert _np(o).tobytes() == e.tobytes()
+    msgs = net.trace
+    assert [m[3] for m in msgs] == case.msgs
+    assert [m[2] for m in msgs] == [len(b) for b in case.msgs]
     assert [m[0] for m in msgs] == list(case.src) and [m[1] for m in msgs] == list(case.dst)
 
 
@@ -41,13 +46,13 @@ SCAT = G.scatter_cases()
 
 @pytest.mark.parametrize("case", SCAT, ids=[f"N{c.N}-root{c.root}" for c in SCAT])
 def test_scatter_matches_reference(case, ws):
-    outs, rep = C.run_collective("binomial-scatter", case.data, ranks=case.N, eb=1e-4, counts=case.counts,
-                                 root=case.root, record_payloads=True, workspace=ws)
+    net = C.create_network(C.CommunicatorSpec(case.N, case.root), record_payloads=True)
+    outs, rep = C.run_collective(net, "binomial-scatter", case.data, eb=1e-4, counts=case.counts, workspace=ws)
     for o, e in zip(outs, case.outputs):
-        assert o.cpu().numpy().tobytes() == e.tobytes()
-    assert [m[2] for m in rep.trace.msgs] == case.msgs
-    assert [m[0] for m in rep.trace.msgs] == list(case.src)
-    assert [m[1] for m in rep.trace.msgs] == list(case.dst)
+        assert _np(o).tobytes() == e.tobytes()
+    assert [m[3] for m in net.trace] == case.msgs
+    assert [m[0] for m in net.trace] == list(case.src)
+    assert [m[1] for m in net.trace] == list(case.dst)
 
 
 OP_COUNT_CASES = [
@@ -63,7 +68,7 @@ def test_op_counts(algo, expect, N, ws):
     # pkg/tests/test_collectives.py:61-80
     rng = np.random.default_rng(N)
     inputs = [rng.uniform(0, 1, 2 * N).astype(np.float32) for _ in range(N)]
-    _, rep = C.run_collective(algo, inputs, eb=1e-4, workspace=ws)
+    _, rep = C.run_collective(N, algo, inputs, eb=1e-4, workspace=ws)
     for c in rep.counters_per_rank:
         assert (c["n_compress"], c["n_decompress"]) == expect(N)
 
@@ -75,29 +80,29 @@ def test_allreduce_error_budget(eb, N, oracle, ws):
     rng = np.random.default_rng(int(N / eb) % 1000)
     n = 50_000
     inputs = [oracle.smooth_field(n, 0.37 * r) + rng.normal(0, 1e-2, n).astype(np.float32) for r in range(N)]
-    outs, _ = C.run_collective("ring-allreduce", inputs, eb=eb, workspace=ws)
+    outs, _ = C.run_collective(N, "ring-allreduce", inputs, eb=eb, workspace=ws)
     lossless = oracle.ring_allreduce(inputs, eb, raw=True)
     for o, e in zip(outs, lossless):
-        assert max_err(e, o.cpu().numpy()) <= N * eb
+        assert max_err(e, _np(o)) <= N * eb
 
 
 def test_errors(ws):
     with pytest.raises(ValueError, match="equal length"):
-        C.run_collective("ring-allreduce", [np.zeros(10, np.float32), np.zeros(11, np.float32)], eb=1e-4, workspace=ws)
+        C.run_collective(2, "ring-allreduce", [np.zeros(10, np.float32), np.zeros(11, np.float32)], eb=1e-4, workspace=ws)
     with pytest.raises(ValueError, match="counts"):
-        C.run_collective("binomial-scatter", np.zeros(10, np.float32), ranks=2, eb=1e-4, counts=[4, 4], workspace=ws)
+        C.run_collective(2, "binomial-scatter", np.zeros(10, np.float32), eb=1e-4, counts=[4, 4], workspace=ws)
     with pytest.raises(ValueError, match="unknown algorithm"):
-        C.run_collective("nope", [np.zeros(4, np.float32)], eb=1e-4)
+        C.run_collective(1, "nope", [np.zeros(4, np.float32)], eb=1e-4)
     with pytest.raises(ValueError, match="unknown reduce op"):
-        C.run_collective("ring-allreduce", [np.zeros(4, np.float32)] * 2, eb=1e-4, reduce_op="prod", workspace=ws)
+        C.run_collective(2, "ring-allreduce", [np.zeros(4, np.float32)] * 2, eb=1e-4, reduce_op="prod", workspace=ws)
 
 
 def test_zero_preservation(ws):
     zeros = [np.zeros(64, np.float32) for _ in range(4)]
     for algo in ("ring-allgather", "ring-reduce-scatter", "ring-allreduce"):
-        outs, _ = C.run_collective(algo, zeros, eb=1e-4, workspace=ws)
+        outs, _ = C.run_collective(4, algo, zeros, eb=1e-4, workspace=ws)
         for o in outs:
-            assert torch.all(o == 0.0)
+            assert np.all(_np(o) == 0.0)
 
 
 @pytest.mark.parametrize("N", [2, 4, 8, 16])
@@ -106,7 +111,7 @@ def test_rd_power_of_two_op_counts(N, ws):
     k = N.bit_length() - 1
     rng = np.random.default_rng(N)
     inputs = [rng.uniform(0, 1, 64).astype(np.float32) for _ in range(N)]
-    _, rep = C.run_collective("rd-allreduce", inputs, eb=1e-4, workspace=ws)
+    _, rep = C.run_collective(N, "rd-allreduce", inputs, eb=1e-4, workspace=ws)
     for c in rep.counters_per_rank:
         assert (c["n_compress"], c["n_decompress"]) == (k, k)
 
@@ -117,7 +122,7 @@ def test_rd_remainder_roles(N, ws):
     pof2, r, k, role, _, _ = C.rd_plan(N)
     rng = np.random.default_rng(N)
     inputs = [rng.uniform(0, 1, 64).astype(np.float32) for _ in range(N)]
-    _, rep = C.run_collective("rd-allreduce", inputs, eb=1e-4, workspace=ws)
+    _, rep = C.run_collective(N, "rd-allreduce", inputs, eb=1e-4, workspace=ws)
     for i, c in enumerate(rep.counters_per_rank):
         got = (c["n_compress"], c["n_decompress"])
         assert got == {"donor": (1, 1), "absorber": (k + 1, k + 1), "direct": (k, k)}[role(i)]
@@ -131,10 +136,10 @@ def test_rd_error_budget(eb, N, oracle, ws):
     for seed in range(3):
         rng = np.random.default_rng(50 * seed + N)
         bufs = [rng.uniform(0, 1, 60).astype(np.float32) for _ in range(N)]
-        outs, _ = C.run_collective("rd-allreduce", bufs, eb=eb, workspace=ws)
+        outs, _ = C.run_collective(N, "rd-allreduce", bufs, eb=eb, workspace=ws)
         lossless = oracle.rd_allreduce(bufs, eb, raw=True)
         for o, e in zip(outs, lossless):
-            assert max_err(e, o.cpu().numpy()) <= bound
+            assert max_err(e, _np(o)) <= bound
 
 
 def _synth_images(images, width, height, seed):
@@ -151,12 +156,12 @@ def test_image_stacking_cfg5(eb, cr, psnr_db, maxerr, oracle, ws):
     # BASELINE.md section 2 (reference measured here): 8 images 512x512, ring-allreduce sum;
     # outputs bit-exact with the oracle, so CR / PSNR / max error reproduce the reference's
     imgs = _synth_images(8, 512, 512, 0)
-    outs, rep = C.run_collective("ring-allreduce", imgs, eb=eb, workspace=ws)
+    outs, rep = C.run_collective(8, "ring-allreduce", imgs, eb=eb, workspace=ws)
     expect = oracle.ring_allreduce(imgs, eb)
     for o, e in zip(outs, expect):
-        assert o.cpu().numpy().tobytes() == e.tobytes()
+        assert _np(o).tobytes() == e.tobytes()
     ref = np.concatenate(oracle.ring_allreduce(imgs, eb, raw=True)).astype(np.float64)
-    got = np.concatenate([o.cpu().numpy() for o in outs]).astype(np.float64)
+    got = np.concatenate([_np(o) for o in outs]).astype(np.float64)
     err = np.abs(ref - got)
     mse = float(np.mean((ref - got) ** 2))
     rng_ = float(ref.max() - ref.min())
@@ -164,15 +169,18 @@ def test_image_stacking_cfg5(eb, cr, psnr_db, maxerr, oracle, ws):
     assert 10 * np.log10(rng_ ** 2 / mse) == pytest.approx(psnr_db, abs=0.05)
     assert float(err.max()) == pytest.approx(maxerr, rel=0.01)
     assert float(err.max()) <= 8 * eb
+    # the report's own accuracy block: the lossless rerun of the same schedule on the device
+    assert rep.accuracy.max_abs_err == pytest.approx(float(err.max()), rel=1e-12)
+    assert rep.accuracy.psnr == pytest.approx(psnr_db, abs=0.05)
 
 
 def test_lossless_scatter_exact(ws):
     rng = np.random.default_rng(5)
     data = rng.normal(0, 1, 1000).astype(np.float32)
-    outs, _ = C.run_collective("lossless-scatter", data, ranks=4, counts=[100, 200, 300, 400], workspace=ws)
+    outs, _ = C.run_collective(4, "lossless-scatter", data, counts=[100, 200, 300, 400], workspace=ws)
     lo = 0
     for o, c in zip(outs, [100, 200, 300, 400]):
-        assert o.cpu().numpy().tobytes() == data[lo:lo + c].tobytes()
+        assert _np(o).tobytes() == data[lo:lo + c].tobytes()
         lo += c
 
 
@@ -182,9 +190,9 @@ def test_cprp2p_hop_error(N, oracle, ws):
     eb = 1e-3
     rng = np.random.default_rng(N)
     chunks = [rng.uniform(0, 1, 100).astype(np.float32) for _ in range(N)]
-    outs, rep = C.run_collective("cprp2p-allgather", chunks, eb=eb, workspace=ws)
+    outs, rep = C.run_collective(N, "cprp2p-allgather", chunks, eb=eb, workspace=ws)
     for i, o in enumerate(outs):
-        o = o.cpu().numpy()
+        o = _np(o)
         for c in range(N):
             h = (i - c) % N
             assert np.max(np.abs(o[100 * c:100 * (c + 1)] - chunks[c])) <= max(h, 0) * eb + 1e-7
