@@ -166,6 +166,13 @@ def _as_device_f32(data, device=None) -> tuple[torch.Tensor, bool]:
     return torch.from_numpy(x).to(dev, non_blocking=False), False
 
 
+def _on(stream):
+    """Run a call's copies and kernels on ``stream`` (default: the current stream)."""
+    import contextlib
+
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
 def compress(data, eb, workspace: Workspace | None = None, *, block: int = BLOCK, return_offsets: bool = False,
              stream=None):
     """Compress binary32 values under an absolute error bound (codec.py:149-270).
@@ -173,8 +180,16 @@ def compress(data, eb, workspace: Workspace | None = None, *, block: int = BLOCK
     Host input -> ``bytes`` (byte-identical to the reference).  CUDA tensor
     input -> :class:`DeviceBlob`.  Host torch tensor (pinned) -> pinned host
     uint8 tensor holding the reference bytes.  Rejects non-finite input (``ValueError``
-    naming the first bad offset) and non-positive bounds.
+    naming the first bad offset) and non-positive bounds.  Every copy and
+    kernel of the call is ordered on ``stream``: calls on distinct streams with
+    distinct workspaces run concurrently (e.g. one host buffer's H2D beside
+    another's D2H).
     """
+    with _on(stream):
+        return _compress(data, eb, workspace, block, return_offsets, stream)
+
+
+def _compress(data, eb, workspace, block, return_offsets, stream):
     _check_block(block)
     ebf = _check_eb(eb)
     x, on_dev = _as_device_f32(data, workspace.device if workspace is not None else None)
@@ -268,8 +283,14 @@ def decompress(blob, workspace: Workspace | None = None, *, stream=None, check: 
     ``bytes``-like input -> ``np.ndarray``; :class:`DeviceBlob` or CUDA uint8
     tensor -> ``torch.Tensor`` on that device; host uint8 tensor -> pinned
     host float32 tensor.  Raises :class:`DecodeError` on
-    malformed headers, truncated payloads or unknown width codes.
+    malformed headers, truncated payloads or unknown width codes.  Ordered on
+    ``stream`` like :func:`compress`.
     """
+    with _on(stream):
+        return _decompress(blob, workspace, stream, check)
+
+
+def _decompress(blob, workspace, stream, check):
     if isinstance(blob, DeviceBlob):
         ws = _ws_for(workspace, blob.data.device)
         return _decode_with_sidecar(blob.data, blob.sidecar, blob.n, blob.eb, ws, stream, check)

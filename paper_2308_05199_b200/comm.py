@@ -132,6 +132,7 @@ class Communicator:
         self.capture_stream = torch.cuda.Stream(self.device)
         self._graph_cache = {}
         self._last_key = None
+        self._seen_keys = set()
         # allgather: "multi" (one launch decodes every owner's blob out of its memory), "copy" (pull each
         # blob over NVLink on a side stream, decode it locally) or "auto" (multi for chunks up to
         # AG_MULTI_MAX values, where it wins by up to ~30 µs per call at N = 4; copy above -- also at
@@ -177,6 +178,7 @@ class Communicator:
         self.epoch = 0
         self._graph_cache = {}
         self._last_key = None
+        self._seen_keys = set()
         dist.barrier(group=self.group)
 
     def _close(self):
@@ -191,6 +193,7 @@ class Communicator:
         self._n = None
         self._graph_cache = {}
         self._last_key = None
+        self._seen_keys = set()
         _scatter_close(self)
         _rd_close(self)
 
@@ -297,7 +300,7 @@ class Communicator:
                 self.graph_launches += g[1]
                 self.launches_per_call = g[1]
                 return
-            if self._n is not None and self._last_key == key and len(self._graph_cache) < 16:
+            if self._n is not None and key in self._seen_keys and len(self._graph_cache) < 16:
                 g = torch.cuda.CUDAGraph()
                 s0 = torch.cuda.current_stream(self.device)
                 with torch.cuda.graph(g, stream=self.capture_stream):
@@ -308,6 +311,7 @@ class Communicator:
                 self.graph_launches += self.launches_per_call
                 return
         self._last_key = key
+        self._seen_keys.add(key)  # a second call with the same key is captured (also when keys alternate)
         self._ring(mode, x, spans, ebf, opc, out)
 
     def ring_reduce_scatter(self, x: torch.Tensor, eb: float, op: str = "sum", out: torch.Tensor | None = None,
