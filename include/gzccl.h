@@ -201,7 +201,7 @@ typedef struct {
  * collective's input that are kept verbatim, never compressed (the scatter
  * root's own block, collectives.py:500), are validated like the rest. */
 int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_base, gz_status* d_status,
-                    gz_stream_t stream);  /* dst == NULL: check only */
+                    gz_stream_t stream);  /* dst == NULL: check only; any 4-byte alignment */
 /* out[n] = op(local, recv): _apply_op (collectives.py:32-39), op 0 = sum (binary32
  * RN), 1 = np.maximum (NaN propagates, ties return recv).  out may alias local. */
 int gz_apply_op(const float* local, const float* recv, float* out, uint64_t n, int op, gz_stream_t stream);

@@ -211,8 +211,19 @@ __global__ void k_copy_blob(const uint4* __restrict__ src, uint4* __restrict__ d
 // the same way the encoder checks everything it compresses.
 __global__ void k_copy_checked(const float4* __restrict__ src, float4* __restrict__ dst, uint64_t n, Status* st,
                                uint64_t report_base) {
-  const uint64_t n4 = n >> 2, stride = (uint64_t)gridDim.x * blockDim.x;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   const uint64_t t0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  if (((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) & 15) != 0) {  // unaligned slice
+    const float* s1 = reinterpret_cast<const float*>(src);
+    float* d1 = reinterpret_cast<float*>(dst);
+    for (uint64_t i = t0; i < n; i += stride) {
+      const float v = s1[i];
+      if (d1) d1[i] = v;
+      if (!isfinite(v)) atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + i));
+    }
+    return;
+  }
+  const uint64_t n4 = n >> 2;
   for (uint64_t i = t0; i < n4; i += stride) {
     const float4 v = __ldcs(src + i);
     if (dst) __stcs(dst + i, v);
@@ -764,7 +775,8 @@ int gz_copy_blob(const uint8_t* src, uint8_t* dst, const uint64_t* d_len, uint64
 int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_base, gz_status* d_status,
                     gz_stream_t stream) {
   if (n == 0) return 0;
-  if (!src || !d_status || !aligned16(src) || (dst && !aligned16(dst))) return GZ_EINVAL;
+  if (!src || !d_status || (reinterpret_cast<uintptr_t>(src) & 3) || (reinterpret_cast<uintptr_t>(dst) & 3))
+    return GZ_EINVAL;
   const uint64_t want = ((n >> 2) + 255) / 256;
   const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(want, 4ull * dev_sms(cur_dev())));
   count_launch();
