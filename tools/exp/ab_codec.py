@@ -7,6 +7,22 @@ from oracle import oracle as O
 
 u64, u32, p, dbl = ctypes.c_uint64, ctypes.c_uint32, ctypes.c_void_p, ctypes.c_double
 libs = {}
+persist = int(os.environ.get("PERSIST_MB", "0"))
+if persist:
+    import glob
+    import nvidia.cuda_runtime as _cr
+    cands = glob.glob(os.path.join(os.path.dirname(_cr.__file__), "lib", "libcudart*.so*")) + ["libcudart.so"]
+    for c in cands:
+        try:
+            rt = ctypes.CDLL(c)
+            break
+        except OSError:
+            rt = None
+    torch.cuda.init()
+    rc = rt.cudaDeviceSetLimit(ctypes.c_int(6), ctypes.c_size_t(persist << 20)) if rt else -1
+    v = ctypes.c_size_t(0)
+    rt.cudaDeviceGetLimit(ctypes.byref(v), ctypes.c_int(6))
+    print("persisting L2 limit rc", rc, "now", v.value >> 20, "MB")
 for path in sys.argv[1:]:
     L = ctypes.CDLL(path)
     L.gz_compress.argtypes = [p, u64, dbl, u32, p, u64, p, p, p, p, u64, p, p]
