@@ -1045,3 +1045,5 @@ def _rd_close(self):
 
 
 Communicator.rd_allreduce = rd_allreduce
+
+from . import comm_generic as _comm_generic  # noqa: E402,F401  (comparator collectives, attached to Communicator)

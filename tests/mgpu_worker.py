@@ -228,6 +228,45 @@ def main():
     if got.cpu().numpy().tobytes() != O.ring_allreduce(xs, 1e-4)[rank].tobytes():
         failures.append("allreduce after errors")
     checked += 1
+    # the comparators on the real multi-GPU path (collectives.py:94-194, 311-341): lossless twins,
+    # the fixed-rate transport and the compress-per-hop allgather, vs the single-GPU schedules
+    # (themselves bit-exact vs the reference, tests/test_transport_gpu.py) and the reference goldens
+    from paper_2308_05199_b200 import collectives as C
+    for case in G.ring_cases():
+        if case.N != world or case.algo not in ("lossless-allreduce", "lossless-reduce-scatter",
+                                                "lossless-allgather", "cprp2p-allgather"):
+            continue
+        xin = torch.from_numpy(np.ascontiguousarray(case.inputs[rank], np.float32)).to(dev)
+        for rep in range(2):
+            if case.algo == "lossless-allreduce":
+                got = c.lossless_allreduce(xin, case.op)
+            elif case.algo == "lossless-reduce-scatter":
+                got = c.lossless_reduce_scatter(xin, case.op)
+            elif case.algo == "lossless-allgather":
+                got = c.lossless_allgather(xin)
+            else:
+                got = c.cprp2p_allgather(xin, case.eb)
+            if got.cpu().numpy().tobytes() != np.ascontiguousarray(case.outputs[rank], np.float32).tobytes():
+                failures.append(f"{case.algo} golden N={case.N} rep={rep}")
+            checked += 1
+    for n, op in ((300_007, "sum"), (65_536, "max")):
+        bufs = [O.smooth_field(n, 0.23 * r) + np.random.default_rng(700 + r).normal(0, 1e-2, n).astype(np.float32)
+                for r in range(world)]
+        xin = torch.from_numpy(bufs[rank]).to(dev)
+        for algo, codec, fn in (("lossless-allreduce", "ebz", lambda: c.lossless_allreduce(xin, op)),
+                                ("ring-allreduce", "fixed-rate", lambda: c.fixed_rate_allreduce(xin, 9, op)),
+                                ("lossless-reduce-scatter", "ebz", lambda: c.lossless_reduce_scatter(xin, op)),
+                                ("ring-reduce-scatter", "fixed-rate",
+                                 lambda: c.generic_reduce_scatter(xin, "fixed-rate", bits=9, op=op)),
+                                ("ring-allgather", "fixed-rate", lambda: c.generic_allgather(xin, "fixed-rate", bits=9)),
+                                ("cprp2p-allgather", "ebz", lambda: c.cprp2p_allgather(xin, 1e-3))):
+            ref_out, _ = C.run_collective(world, algo, bufs, eb=1e-3, codec=codec, bits=9, reduce_op=op,
+                                          compute_accuracy=False)
+            for rep in range(2):
+                got = fn()
+                if got.cpu().numpy().tobytes() != np.ascontiguousarray(ref_out[rank], np.float32).tobytes():
+                    failures.append(f"{algo}/{codec} n={n} op={op} rep={rep}")
+                checked += 1
     flag = torch.tensor([len(failures)], device="cpu" if oversub else dev)
     dist.all_reduce(flag)
     if rank == 0:

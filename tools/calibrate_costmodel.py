@@ -64,6 +64,8 @@ def fit(points):
     x = np.array([b for b, _ in big], float)
     y = np.array([t for _, t in big], float)
     slope, icpt = np.polyfit(x, y, 1)
+    if slope <= 0:  # no size-proportional cost (e.g. the fused step's extra over compress + decompress)
+        return max(float(np.median(y)), 1e-7), 1.0, 1e15
     thr = 1.0 / slope
     launch = max(icpt, 1e-7)
     plateau = min(t for b, t in points if b <= (1 << 20))

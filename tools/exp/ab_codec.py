@@ -29,6 +29,7 @@ for path in sys.argv[1:]:
     L.gz_compress_bound.restype = L.gz_workspace_bytes.restype = L.gz_sidecar_bytes.restype = u64
     L.gz_compress_bound.argtypes = L.gz_workspace_bytes.argtypes = L.gz_sidecar_bytes.argtypes = [u64]
     L.gz_workspace_init.argtypes = [p, u64, p]
+    L.gz_decompress_sidecar.argtypes = [p, p, u64, dbl, p, p, p]
     libs[os.path.basename(path)] = L
 s = torch.cuda.current_stream()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
@@ -56,4 +57,19 @@ for n in (1 << 24, 1 << 27):
             if it >= 2:
                 ts.append(a.elapsed_time(b) * 1e3)
         ts.sort()
-        print(f"n=2^{n.bit_length()-1} {name:24s} compress median {ts[len(ts)//2]:8.1f} us  min {ts[0]:8.1f}  len {int(st[4].item())}")
+        y = torch.empty(n, dtype=torch.float32, device="cuda")
+        td = []
+        for it in range(12):
+            if n == 1 << 24:
+                flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            rc = L.gz_decompress_sidecar(blob.data_ptr(), sc.data_ptr(), n, 1e-4, y.data_ptr(), st.data_ptr(), s.cuda_stream)
+            b.record(s)
+            torch.cuda.synchronize()
+            assert rc == 0, rc
+            if it >= 2:
+                td.append(a.elapsed_time(b) * 1e3)
+        td.sort()
+        print(f"n=2^{n.bit_length()-1} {name:24s} compress median {ts[len(ts)//2]:8.1f} us  min {ts[0]:8.1f}  len {int(st[4].item())}"
+              f" | decompress median {td[len(td)//2]:8.1f} min {td[0]:8.1f}")
