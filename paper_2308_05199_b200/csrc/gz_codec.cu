@@ -633,7 +633,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
         m.ts = a.in_tile_off[jn];
         m.te = a.in_tile_off[jn + 1];
       }
-      if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;  // corrupt sidecar
       m.w = a.in_w[(uint64_t)jn * TB + lane];
     }
     return m;
@@ -650,6 +649,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     InMeta m_nxt{0, 0, 0};
     if (ONEBUF) {
       m_nxt = load_meta(j1);
+      if (m_cur.te < m_cur.ts || m_cur.te - m_cur.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m_cur.te = m_cur.ts;  // corrupt sidecar
       in_cur.base = stage_bytes<true>(stg0, in_base, m_cur.ts, m_cur.te, lane);
       in_cur.bytes = (int)(m_cur.te - m_cur.ts);
       in_cur.w = m_cur.w;
@@ -960,18 +960,19 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
         m.ts = S.tile_off[lt];
         m.te = S.tile_off[lt + 1];
       }
-      // a corrupt sidecar must not overflow the staging buffer: stage nothing,
-      // block_start() then reports the mismatch
-      if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;
     }
     return m;
   };
   // stage tile t into buffer bi (cp.async, caller commits); returns base, width
-  auto stage = [&](uint64_t t, const Meta& m, int bi, int& base, int& w) {
+  auto stage = [&](uint64_t t, Meta& m, int bi, int& base, int& w) {
     base = 0;
     w = 0;
     if (t < total) {
       const DecSeg& S = a.seg[seg_of(t)];
+      // a corrupt sidecar must not overflow the staging buffer: stage nothing,
+      // block_start() then reports the mismatch (checked here, where the offsets
+      // are consumed, so their loads stay in flight behind the previous tile)
+      if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;
       base = stage_bytes<true>(stg + bi * STAGE_WORDS, S.sizes ? S.blob : S.blob + HEADER_BYTES, m.ts, m.te, lane);
       w = S.widths[(t - S.tile_base) * TB + lane];
     }
