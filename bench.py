@@ -399,7 +399,7 @@ def bench_codec(args):
 
     # e2e through the public API with pinned host buffers, two steps in flight
     xp = torch.from_numpy(xh).pin_memory()
-    lanes = 2
+    lanes = 3  # steps in flight (tools/exp/e2e_lanes.py: 49 / 64 / 77 GB/s for 1 / 2 / 3, 4 collapses)
     e2e_ws = [gz.Workspace(dev) for _ in range(lanes)]
     e2e_streams = [torch.cuda.Stream(dev) for _ in range(lanes)]
     e2e_steps = max(8, min(args.steps, 20))

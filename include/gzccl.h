@@ -140,7 +140,9 @@ typedef struct {
                           the peers' streams drain instead of hanging */
   uint64_t report_base; /* added to the offset of a non-finite value of `local` before it is recorded
                            in d_status->first_nonfinite (the chunk's offset in the caller's buffer,
-                           so the first bad offset of the whole buffer is reported, codec.py:79-86) */
+                           so the first bad offset of the whole buffer is reported, codec.py:79-86);
+                           UINT64_MAX: `local` is not the caller's input (e.g. reduced in place by an
+                           earlier step), report nothing */
 } gz_step_io;
 uint64_t gz_slots_bytes(uint64_t m);
 int gz_step(const gz_step_io* io, const float* local, uint64_t m, double eb, int op, float* acc_out, void* ws,

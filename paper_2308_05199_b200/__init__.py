@@ -27,6 +27,7 @@ from .codec import (
 )
 from .collectives import CommunicatorSpec, Network, create_network, run_collective
 from .collectives import Counters as OpCounters
+from .costmodel import CostParams, b200_cost_params, load_cost_params, predicted_makespan
 from .metrics import AccuracyStats, CollectiveReport, compression_ratio, max_abs_error, psnr
 
 __version__ = "0.1.0"
@@ -35,6 +36,10 @@ __all__ = [
     "AccuracyStats",
     "CollectiveReport",
     "CommunicatorSpec",
+    "CostParams",
+    "b200_cost_params",
+    "load_cost_params",
+    "predicted_makespan",
     "Network",
     "OpCounters",
     "compression_ratio",

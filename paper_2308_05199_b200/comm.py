@@ -42,6 +42,7 @@ from .schedule import Compress, Reduce, ring_allreduce_plan
 
 _ALIGN = 256
 _MAX_DECODE_SEGMENTS = 8  # GZ_MAX_DECODE_SEGMENTS (include/gzccl.h)
+_NO_REPORT = (1 << 64) - 1  # gz_step_io.report_base: `local` is not the caller's input
 AG_COPY_SMS = 24  # SMs left to the allgather's NVLink pulls while the previous owner's blob is decoded
 AG_MULTI_MAX = 8 << 20  # chunk values up to which the allgather decodes every owner in one remote-read launch
 
@@ -994,6 +995,7 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None, check: bool = Tr
         wait(lay.consumed(k), prev)  # rr consumed our message k of the previous call
         io = _StepIO()
         io.out_slots, io.out_sizes, io.out_widths = msg(i, k)
+        io.report_base = 0 if data[0] == x.data_ptr() else _NO_REPORT  # only x is the caller's input
         acc = None
         if src is not None:
             io.in_slots, io.in_sizes, io.in_widths = msg(src, k_in)
@@ -1008,6 +1010,7 @@ def rd_allreduce(self, x, eb: float, op: str = "sum", out=None, check: bool = Tr
         nonlocal launches
         io = _StepIO()
         io.in_slots, io.in_sizes, io.in_widths = msg(src, k_in)
+        io.report_base = 0 if data[0] == x.data_ptr() else _NO_REPORT
         L.check(lib.gz_step_reduce(ctypes.byref(io), data[0] if reduce else None, n, ebf, opc, out.data_ptr(),
                                    ws.status_ptr(), s), "gz_step_reduce")
         launches += 1

@@ -277,26 +277,26 @@ def cprp2p_allgather(self, chunk: torch.Tensor, eb: float, check: bool = True):
     """cprp2p_allgather (collectives.py:311-341): the compress-per-hop baseline.
     At hop s rank i compresses the chunk it received at hop s-1 (its own at
     s = 0) and its right neighbour decodes it: a chunk that travelled h hops
-    carries up to h * eb of error.  Equal chunk lengths."""
+    carries up to h * eb of error.  Chunks may differ in length."""
     chunk, ebf, _ = _prepare(self, chunk, "ebz", eb, 8, "sum")
     N, i = self.world, self.rank
-    m = chunk.numel()
     counts = [None] * N
-    dist.all_gather_object(counts, int(m), group=self.group)
-    if len(set(counts)) > 1:
-        raise ValueError(f"per-rank buffers must have equal length, got {sorted(set(counts))}")
-    out = torch.empty(N * m, dtype=torch.float32, device=self.device)
+    dist.all_gather_object(counts, int(chunk.numel()), group=self.group)
+    lo = [0]
+    for c_ in counts:
+        lo.append(lo[-1] + c_)
+    out = torch.empty(lo[-1], dtype=torch.float32, device=self.device)
     self.ws.reset_status()
-    self._copy_checked(chunk, out[i * m:(i + 1) * m], reset=False)
+    self._copy_checked(chunk, out[lo[i]:lo[i + 1]], reset=False)
     if N > 1:
-        _setup(self, "ebz", m, 8)
+        _setup(self, "ebz", max(counts), 8)
         ring = _Ring(self, "ebz", ebf, 8, "sum")
         right, left = (i + 1) % N, (i - 1) % N
         cur = i
         for s in range(N - 1):
-            ring.send(s, out[cur * m:(cur + 1) * m], [right])
+            ring.send(s, out[lo[cur]:lo[cur + 1]], [right])
             cur = (i - 1 - s) % N
-            ring.recv(s, left, out[cur * m:(cur + 1) * m], reduce=False)
+            ring.recv(s, left, out[lo[cur]:lo[cur + 1]], reduce=False)
         ring.done()
     if check:
         self.check()

@@ -14,6 +14,9 @@
 namespace gz {
 
 enum { SRC_PLAIN = 0, SRC_STEP = 1 };
+// report_base value of a kernel whose `local` is NOT the caller's input (e.g. a
+// recursive-doubling step reducing into its output in place): nothing is reported
+constexpr uint64_t NO_REPORT = ~0ull;
 enum { OP_SUM = 0, OP_MAX = 1 };
 
 // One independently compressed blob (a compress_blocks segment).
@@ -157,7 +160,7 @@ __device__ __forceinline__ void drain_values_op(const float* xs, const float* __
     bad |= !isfinite(l);
     __stcs(dst + v0 + i, op == 0 ? __fadd_rn(l, d) : np_maximum_f(l, d));
   }
-  if (__any_sync(0xFFFFFFFFu, bad)) {
+  if (__any_sync(0xFFFFFFFFu, bad) && report_base != NO_REPORT) {
     for (int i = lane; i < nval; i += 32)
       if (!isfinite(local[v0 + i])) atomicMin(&st->first_nonfinite, (unsigned long long)(report_base + v0 + i));
   }
@@ -449,7 +452,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
       uint32_t zl[32];
       zor = slow_block(row, cnt, a.qp, zl, &flags);
       store_codes(zs, lane, x0, zl);
-      if (flags & 4) {  // codec.py:83-85: report the first non-finite offset of the caller's buffer
+      if ((flags & 4) && S.report_base != NO_REPORT) {  // codec.py:83-85: the first non-finite offset of the caller's buffer
         // (in the fused step the values are op(local, received): only `local` is this rank's input)
         const float* src = S.x + v0 + (uint64_t)lane * 32;
         for (int j = 0; j < cnt; ++j)

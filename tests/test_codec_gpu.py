@@ -253,3 +253,49 @@ def test_truncation_exactly_at_a_segment_boundary(cut_segments, oracle, ws):
         gz.decompress(blob[:cut], ws)
     with pytest.raises(gz.DecodeError, match=msg):
         gz.decompress(torch.frombuffer(bytearray(blob[:cut]), dtype=torch.uint8).cuda(), ws)
+
+
+@pytest.mark.parametrize("slotted_in", [True, False])
+def test_fused_step_reports_nonfinite_local_offset(slotted_in, oracle, ws):
+    # every kernel that reads a collective's input records the first non-finite offset of
+    # the caller's buffer (codec.py:79-86): the fused step checks `local` (+ report_base),
+    # not the received values
+    import ctypes
+    from paper_2308_05199_b200 import _lib as L
+    from paper_2308_05199_b200.comm import _StepIO
+
+    lib = L.lib()
+    n = 100_003
+    a = oracle.smooth_field(n)
+    b = oracle.smooth_field(n, 0.4)
+    b[54_321] = np.nan
+    b[99_000] = np.inf
+    at, bt = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    nt = int(lib.gz_num_tiles(n))
+    s = torch.cuda.current_stream().cuda_stream
+    tws = ws.tile_ws(int(lib.gz_workspace_bytes(n)))
+
+    def slots():
+        sl = torch.empty(int(lib.gz_slots_bytes(n)) + 128, dtype=torch.uint8, device="cuda")
+        return sl, (sl.data_ptr() + 127) & ~127, torch.empty(nt, dtype=torch.int32, device="cuda"), \
+            torch.empty(32 * nt, dtype=torch.uint8, device="cuda")
+    s_in, s_out = slots(), slots()
+    io = _StepIO()
+    io.out_slots, io.out_sizes, io.out_widths = s_in[1], s_in[2].data_ptr(), s_in[3].data_ptr()
+    ws.reset_status()
+    L.check(lib.gz_step(ctypes.byref(io), at.data_ptr(), n, 1e-4, 0, None, tws.data_ptr(), tws.numel(),
+                        ws.status_ptr(), s), "gz_step")
+    assert ws.read_status()[0] == (1 << 64) - 1
+    blob = gz.compress(at, 1e-4, ws)
+    io2 = _StepIO()
+    if slotted_in:
+        io2.in_slots, io2.in_sizes, io2.in_widths = s_in[1], s_in[2].data_ptr(), s_in[3].data_ptr()
+    else:
+        io2.in_blob, io2.in_sidecar = blob.data.data_ptr(), blob.sidecar.data_ptr()
+    io2.out_slots, io2.out_sizes, io2.out_widths = s_out[1], s_out[2].data_ptr(), s_out[3].data_ptr()
+    io2.report_base = 1000
+    acc = torch.empty(n, dtype=torch.float32, device="cuda")
+    ws.reset_status()
+    L.check(lib.gz_step(ctypes.byref(io2), bt.data_ptr(), n, 1e-4, 0, acc.data_ptr(), tws.data_ptr(), tws.numel(),
+                        ws.status_ptr(), s), "gz_step")
+    assert int(ws.read_status()[0]) == 1000 + 54_321
