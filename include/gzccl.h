@@ -90,6 +90,14 @@ int gz_decompress_reduce(const uint8_t* blob, const void* sidecar, const float* 
 int gz_decompress_multi(const uint8_t* const* blobs, const void* const* sidecars, const uint64_t* ns, uint32_t count,
                         double eb, float* const* ys, int reserve_sms, gz_status* d_status, gz_stream_t stream);
 
+/* The same for messages in slotted form (gz_step_io's out_slots / out_sizes /
+ * out_widths, 128-byte aligned slots; usually a peer GPU's memory): the
+ * compress-once allgather decoding every owner's last reduce-scatter output in
+ * place, without first gathering it into a contiguous blob. */
+int gz_decompress_slots_multi(const uint8_t* const* slots, const uint32_t* const* sizes, const uint8_t* const* widths,
+                              const uint64_t* ns, uint32_t count, double eb, float* const* ys, int reserve_sms,
+                              gz_status* d_status, gz_stream_t stream);
+
 /* gz_index replaces the sequential block walk of codec.decompress
  * (codec.py:298-322): validates the payload of a blob of header count n and
  * payload length payload_len (device pointer to the blob) and builds its

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgzccl.so")
+LIB_PATH = os.environ.get("GZCCL_LIB") or os.path.join(HERE, "libgzccl.so")  # override: A/B experiments
 
 GZ_OK = 0
 GZ_EINVAL = 10001
@@ -32,6 +32,7 @@ SIGNATURES = {
     "gz_decompress_sidecar": (i32, [p, p, u64, dbl, p, p, p]),
     "gz_decompress_reduce": (i32, [p, p, p, u64, dbl, i32, p, p, p]),
     "gz_decompress_multi": (i32, [p, p, p, u32, dbl, p, i32, p, p]),
+    "gz_decompress_slots_multi": (i32, [p, p, p, p, u32, dbl, p, i32, p, p]),
     "gz_index": (i32, [p, u64, u64, p, p, u64, p, p]),
     "gz_index_workspace_bytes": (u64, [u64]),
     "gz_reduce_step": (i32, [p, p, p, u64, dbl, i32, p, p, u64, p, p, p, u64, p, p]),

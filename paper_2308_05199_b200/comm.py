@@ -84,6 +84,15 @@ class _Layout:
             off += self.blob_cap + self.sc_bytes
         self.own_off = (off, off + self.blob_cap)
         off += self.blob_cap + self.sc_bytes
+        # the owned chunk's compress-once message in slotted form (ag_mode "slots"): the last
+        # reduce-scatter step writes it without a gather, the peers decode it in place
+        sl = off
+        off += self.slots_bytes
+        sz = off
+        off += _al(4 * nt)
+        wd = off
+        off += _al(32 * nt)
+        self.own_slot = (sl, sz, wd)
         self.total = off
 
     def rs_full(self, s):
@@ -134,11 +143,12 @@ class Communicator:
         self._graph_cache = {}
         self._last_key = None
         self._seen_keys = set()
-        # allgather: "multi" (one launch decodes every owner's blob out of its memory), "copy" (pull each
-        # blob over NVLink on a side stream, decode it locally) or "auto" (multi for chunks up to
-        # AG_MULTI_MAX values, where it wins by up to ~30 µs per call at N = 4; copy above -- also at
-        # N = 2, where it beats decoding the single owner's blob out of peer memory by ~2.5 % at 512 MiB)
-        self.ag_mode = "auto"
+        # allgather: "slots" (default: the owner's last reduce-scatter step leaves its message in slotted
+        # form -- no gather kernel on the critical path -- and every peer decodes the owners' slots in
+        # place over NVLink, one launch per 8 owners), or the blob-based modes: "multi" (one launch
+        # decodes every owner's blob out of its memory), "copy" (pull each blob over NVLink on a side
+        # stream, decode it locally) and "auto" (multi up to AG_MULTI_MAX values, copy above)
+        self.ag_mode = "slots"
         # intermediate reduce-scatter steps take their input flag inside the kernel (one CTA
         # thread polls, bounded) instead of a stream wait node: ~5 µs less per step
         self.kernel_waits = True
@@ -534,6 +544,11 @@ class Communicator:
                              post=(p.dst, lay.rs_full(p.slot + 1)),
                              wait=lay.rs_full(p.slot) if self.kernel_waits else None, base=spans[p.chunk][0])
                         launches += 1
+                    elif self.ag_mode == "slots":
+                        wait_own_blob_free()  # our own message is read by every peer in the allgather
+                        step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), chunk_ptr(out, p.chunk),
+                             out_slot=tuple(self._addr(i, o) for o in lay.own_slot), base=spans[p.chunk][0])
+                        launches += 1
                     else:
                         wait_own_blob_free()  # our own blob is read by every peer in the allgather
                         step(inp, chunk_ptr(x, p.chunk), msize(p.chunk), chunk_ptr(out, p.chunk),
@@ -547,10 +562,14 @@ class Communicator:
         if mode == "allgather":
             # compress our chunk once into our own blob; the own chunk is kept verbatim
             wait_own_blob_free()
-            L.check(lib.gz_compress(x.data_ptr(), x.numel(), ebf, 32, self._addr(i, lay.own_off[0]), lay.blob_cap,
-                                    self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1]), None,
-                                    tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_compress")
-            launches += 2
+            if self.ag_mode == "slots":
+                step(None, x.data_ptr(), x.numel(), None, out_slot=tuple(self._addr(i, o) for o in lay.own_slot))
+                launches += 1
+            else:
+                L.check(lib.gz_compress(x.data_ptr(), x.numel(), ebf, 32, self._addr(i, lay.own_off[0]), lay.blob_cap,
+                                        self._addr(i, lay.len_off + 8 * N), self._addr(i, lay.own_off[1]), None,
+                                        tws.data_ptr(), tws.numel(), ws.status_ptr(), s), "gz_compress")
+                launches += 2
             self._mark("compress")
             own_ready()
             if x.numel():
@@ -579,6 +598,25 @@ class Communicator:
         ws = self.ws
         launches = 0
         mode = self.ag_mode
+        if mode == "slots":
+            # every owner's slotted message decoded in place (peer memory), 8 owners per launch
+            self._take_all([lay.ag_ready(j) for j in owners], s)
+            nl = 0
+            for g0 in range(0, len(owners), _MAX_DECODE_SEGMENTS):
+                grp = owners[g0:g0 + _MAX_DECODE_SEGMENTS]
+                k = len(grp)
+                P = ctypes.c_void_p * k
+                sls = P(*[self._addr(j, lay.own_slot[0]) for j in grp])
+                szs = P(*[self._addr(j, lay.own_slot[1]) for j in grp])
+                wds = P(*[self._addr(j, lay.own_slot[2]) for j in grp])
+                ns = (ctypes.c_uint64 * k)(*[msize(chunk_of(j)) for j in grp])
+                ys = P(*[chunk_ptr(out, chunk_of(j)) for j in grp])
+                L.check(lib.gz_decompress_slots_multi(sls, szs, wds, ns, k, ebf, ys, 0, ws.status_ptr(), s),
+                        "gz_decompress_slots_multi")
+                nl += 1
+            self._mark("decode")
+            self._post_all([(j, lay.ag_consumed(i)) for j in owners], s)
+            return nl
         if mode == "auto":
             mode = "multi" if max(msize(chunk_of(j)) for j in owners) <= AG_MULTI_MAX else "copy"
         if len(owners) > 1 and mode == "multi":
@@ -675,10 +713,15 @@ class Communicator:
         """Compressed size of this rank's owned chunk (last call), as a ratio."""
         lay = self.layout
         torch.cuda.synchronize(self.device)
-        ln = self._buf[lay.len_off + 8 * self.world : lay.len_off + 8 * self.world + 8].view(torch.int64).item()
         i = self.rank
         c = (i + 1) % self.world
         m = self.spans[c][1] - self.spans[c][0]
+        if self.ag_mode == "slots":  # the owned message's tile sizes
+            nt = int(L.lib().gz_num_tiles(m))
+            sz = self._buf[lay.own_slot[1]:lay.own_slot[1] + 4 * nt].view(torch.int32)
+            ln = int(sz.sum().item()) + 24  # the reference blob = header + payload
+        else:
+            ln = self._buf[lay.len_off + 8 * self.world : lay.len_off + 8 * self.world + 8].view(torch.int64).item()
         self.last_compression_ratio = round(4 * m / ln, 4) if ln else None
         return self.last_compression_ratio
 

@@ -450,6 +450,30 @@ int gz_decompress_multi(const uint8_t* const* blobs, const void* const* sidecars
   return launch_decode<GZ_MAX_DECODE_SEGMENTS>(a, (cudaStream_t)stream, reserve_sms);
 }
 
+int gz_decompress_slots_multi(const uint8_t* const* slots, const uint32_t* const* sizes, const uint8_t* const* widths,
+                              const uint64_t* ns, uint32_t count, double eb, float* const* ys, int reserve_sms,
+                              gz_status* d_status, gz_stream_t stream) {
+  if (!check_eb(eb)) return GZ_EBOUND;
+  if (!slots || !sizes || !widths || !ns || !ys || !d_status || count > GZ_MAX_DECODE_SEGMENTS) return GZ_EINVAL;
+  DecodeMultiArgs<GZ_MAX_DECODE_SEGMENTS> a;
+  std::memset(&a, 0, sizeof(a));
+  uint64_t tiles = 0;
+  int k = 0;
+  for (uint32_t i = 0; i < count; ++i) {
+    if (ns[i] == 0) continue;
+    if (!slots[i] || !sizes[i] || !widths[i] || !ys[i] || (reinterpret_cast<uintptr_t>(slots[i]) & 127)) return GZ_EINVAL;
+    a.seg[k++] = DecSeg{slots[i], nullptr, widths[i], ns[i], ys[i], tiles, sizes[i]};
+    tiles += ntiles_of(ns[i]);
+  }
+  if (k == 0) return 0;
+  a.nseg = k;
+  a.total_tiles = tiles;
+  a.tw = 2.0 * eb;
+  a.st = reinterpret_cast<Status*>(d_status);
+  // the slots are usually in peer GPUs' memory: the three-stage (two tiles ahead) decoder
+  return launch_decode<GZ_MAX_DECODE_SEGMENTS>(a, (cudaStream_t)stream, reserve_sms);
+}
+
 uint64_t gz_index_workspace_bytes(uint64_t payload_len) {
   const uint64_t nseg = (payload_len + SEG - 1) / SEG;
   const uint64_t nch = (nseg + CH - 1) / CH;

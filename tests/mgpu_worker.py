@@ -58,7 +58,7 @@ def main():
                 for r in range(world)]
         expect = O.ring_allreduce(bufs, eb, op)
         x = torch.from_numpy(bufs[rank]).to(dev)
-        for mode in ("copy", "multi", "auto"):  # the allgather's two data paths
+        for mode in ("slots", "copy", "multi", "auto"):  # the allgather's data paths
             c.ag_mode = mode
             c.kernel_waits = mode != "copy"  # ring flags taken by stream wait nodes or inside the kernels
             out = c.ring_allreduce(x, eb, op)
@@ -66,7 +66,7 @@ def main():
             if out.cpu().numpy().tobytes() != expect[rank].tobytes():
                 failures.append(f"oracle n={n} op={op} eb={eb} ag_mode={mode}")
             checked += 1
-    c.ag_mode = "auto"
+    c.ag_mode = "slots"
     c.kernel_waits = True
     # repeated calls on the same tensors are replayed from a captured CUDA graph
     n = 3_000_017
@@ -75,7 +75,7 @@ def main():
     expect = O.ring_allreduce(bufs, 1e-4, "sum")[rank].tobytes()
     expect0 = expect
     expect1 = O.ring_allreduce([bufs[(r + 1) % world] for r in range(world)], 1e-4, "sum")[rank].tobytes()
-    for mode in ("copy", "multi"):
+    for mode in ("slots", "copy", "multi"):
         c.ag_mode = mode
         x = torch.from_numpy(bufs[rank]).to(dev)
         out = torch.empty_like(x)
@@ -89,7 +89,7 @@ def main():
             if out.cpu().numpy().tobytes() != expect:
                 failures.append(f"graph replay rep={rep} ag_mode={mode}")
             checked += 1
-    c.ag_mode = "auto"
+    c.ag_mode = "slots"
     if not c._graph_cache:
         failures.append("no graph was captured")
     # standalone reduce-scatter and allgather(v) (collectives.py:247-291), vs the oracle,
