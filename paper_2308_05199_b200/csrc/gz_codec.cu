@@ -403,32 +403,73 @@ __device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg&
   }
 }
 
-// Stages 3-4 of one warp tile whose quantisation is done (codes in zs, or
-// the block is raw): sizes (codec.py:231-239), the warp scan of the block
-// sizes (codec.py:241-243), packing into `dst` (a 128-byte aligned global
-// slot; the word straddling two blocks is completed by the earlier block with
-// the next block's leading bytes), and the sidecar entries.  Returns the
-// tile's compressed size.
-struct QOut {
-  uint32_t zor;  // OR of the block's zigzag codes (its width, codec.py:224-229)
-  int flags;     // bit0 overflow, bit1 error > eb, bit2 non-finite
-  float x0;      // the block's first value
-};
-
-template <int SRC, int NSEG>
-__device__ __forceinline__ int pack_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
-                                         const float* xs, const float* zs, uint32_t* dst, const QOut& q,
-                                         const uint32_t* stage, int base, int in_start, int in_w, const double* s_step,
-                                         uint64_t pol_keep, int lane) {
+// Phase A for one warp tile (values in xs): quantise and pack the tile into
+// `dst` starting at byte `pos0`.  In a run (carry mode) the tile continues the
+// previous tile's bytes: `carry` holds that tile's last partial word and the
+// function returns this tile's, instead of completing it with zeros.
+template <int SRC, int NSEG, bool FAST>
+__device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
+                                           float* xs, uint32_t* dst, int pos0, bool run_mode, uint32_t& carry,
+                                           uint32_t* stage, int in_base, int in_bytes, int in_w,
+                                           const double* s_step, uint64_t pol_keep, int lane) {
   const uint64_t nb = G.nb, b0 = tile * TB, v0 = b0 * BLOCK;
+  const int last_cnt = G.last_cnt;
   const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
+  const int nval = (int)(G.n - v0 < (uint64_t)TILE_VALUES ? G.n - v0 : (uint64_t)TILE_VALUES);
+  int base = 0, in_start = -1;
+
+  // ---- 1. fused step: combine the received blob's tile into xs
+  // (its compressed bytes were staged asynchronously with the local values)
+  if (SRC == SRC_STEP) {
+    base = in_base;
+    in_start = block_start(stage, base, in_bytes, in_w, nblk, b0, nb, last_cnt, a.st, lane);
+    __syncwarp();
+    decode_row<1>(stage, base, in_start, in_w, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, lane);
+    __syncwarp();
+    if (a.acc_out) drain_values(xs, a.acc_out, v0, nval, lane);
+    __syncwarp();
+  }
+
+  // ---- 2. closed-loop quantisation, one lane per 32-value block; the codes
+  // replace the values in the lane's shared-memory row -- except in the fused
+  // step, whose consumed staging buffer takes them, so that the rare raw or
+  // unproven block still finds its values (local + received) in xs
+  __syncwarp();
+  float* zs = SRC == SRC_STEP ? reinterpret_cast<float*>(stage) : xs;
   const bool active = lane < nblk;
-  const int cnt = active ? ((b0 + lane == nb - 1) ? G.last_cnt : 32) : 0;
-  const int w = 32 - __clz(q.zor);                                 // codec.py:224-229
+  const int cnt = active ? ((b0 + lane == nb - 1) ? last_cnt : 32) : 0;
+  uint32_t zor = 0;
+  int flags = 0;
+  float x0 = 0.0f;
+  if (active) {
+    int fb = FB_SLOW;
+    if (FAST && cnt == 32) fb = fast_block(xs, zs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
+    if (fb == FB_SLOW) {  // rare: exact replay of the whole block
+      float row[32];
+      if (FAST && cnt == 32 && zs == xs) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
+      else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
+      x0 = row[0];
+      uint32_t zl[32];
+      zor = slow_block(row, cnt, a.qp, zl, &flags);
+      store_codes(zs, lane, x0, zl);
+      if ((flags & 4) && S.report_base != NO_REPORT) {  // codec.py:83-85: the first non-finite offset of the caller's buffer
+        // (in the fused step the values are op(local, received): only `local` is this rank's input)
+        const float* src = S.x + v0 + (uint64_t)lane * 32;
+        for (int j = 0; j < cnt; ++j)
+          if (!isfinite(SRC == SRC_STEP ? src[j] : row[j])) {
+            atomicMin(&a.st->first_nonfinite, (unsigned long long)(S.report_base + v0 + (uint64_t)lane * 32 + j));
+            break;
+          }
+      }
+    } else if (fb == FB_RAW) {
+      flags |= 2;
+    }
+  }
+  const int w = 32 - __clz(zor);                                   // codec.py:224-229
   const int ncodes = cnt - 1;
   const int packed = 5 + (ncodes * w + 7) / 8;                     // 236
   const int rawsz = 1 + 4 * cnt;                                   // 237
-  const bool raw = (q.flags & 3) || packed > rawsz;                // 238
+  const bool raw = (flags & 3) || packed > rawsz;                  // 238
   const int size = active ? (raw ? rawsz : packed) : 0;            // 239
   const int wbyte = raw ? RAW_WIDTH : w;
 
@@ -445,22 +486,24 @@ __device__ __forceinline__ int pack_tile(const EncodeArgs<NSEG>& a, const Seg& S
   // ---- 4. pack into dst; the word straddling two blocks is completed by
   // the earlier block with the next block's leading bytes
   const uint32_t next_w = __shfl_down_sync(0xFFFFFFFFu, (uint32_t)wbyte, 1);
-  const uint32_t next_x0 = __shfl_down_sync(0xFFFFFFFFu, __float_as_uint(q.x0), 1);
+  const uint32_t next_x0 = __shfl_down_sync(0xFFFFFFFFu, __float_as_uint(x0), 1);
+  uint32_t my_carry = 0;
   if (active) {
     Appender ap;
-    ap.init(dst, start, lane == 0);
+    if (lane == 0 && run_mode) ap.init_carry(dst, pos0, carry);
+    else ap.init(dst, pos0 + start, lane == 0);
     ap.pol = pol_keep;
     if (raw) {
       float row[32];
       if (zs == xs) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
       else load_row(xs, lane, *reinterpret_cast<float(*)[32]>(row));
-      ap.append(255ull | ((uint64_t)__float_as_uint(q.x0) << 8), 5);
+      ap.append(255ull | ((uint64_t)__float_as_uint(x0) << 8), 5);
       int j = 1;
       for (; j + 1 < cnt; j += 2)
         ap.append((uint64_t)__float_as_uint(row[j]) | ((uint64_t)__float_as_uint(row[j + 1]) << 32), 8);
       if (j < cnt) ap.append((uint64_t)__float_as_uint(row[j]), 4);
     } else {
-      ap.append((uint64_t)w | ((uint64_t)__float_as_uint(q.x0) << 8), 5);
+      ap.append((uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8), 5);
       if (w > 0) {
         uint32_t z[31];
         load_codes(zs, lane, z);
@@ -500,82 +543,14 @@ __device__ __forceinline__ int pack_tile(const EncodeArgs<NSEG>& a, const Seg& S
       }
     }
     if (lane + 1 < nblk) ap.finish((uint64_t)next_w | ((uint64_t)next_x0 << 8));
-    else ap.finish(0ull);
+    else if (!run_mode) ap.finish(0ull);
+    else my_carry = ap.pend;  // the run's next tile completes this word
   }
+  carry = __shfl_sync(0xFFFFFFFFu, my_carry, nblk > 0 ? nblk - 1 : 0);
   // block widths (the sidecar; independent of the tile's position)
   if (active && S.out_w) S.out_w[b0 + lane] = (uint8_t)wbyte;
   if (active && a.blk_off) a.blk_off[b0 + lane] = (unsigned long long)start;  // made absolute in phase B
   return tile_bytes;
-}
-
-// Exact replay of one block whose fast pass was not conclusive (rare), and the
-// report of its first non-finite input value (codec.py:83-85, an offset in the
-// caller's buffer; in the fused step the values are op(local, received) and
-// only `local` is this rank's input).
-template <int SRC, int NSEG>
-__device__ __forceinline__ void slow_replay(const EncodeArgs<NSEG>& a, const Seg& S, uint64_t v0, int cnt, const float* row_src,
-                                         bool from_global, float* zs, QOut& q, const uint32_t* stage, int base,
-                                         int in_start, int in_w, const double* s_step, int lane) {
-  float row[32];
-  if (from_global) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
-  else load_row(row_src, lane, *reinterpret_cast<float(*)[32]>(row));
-  q.x0 = row[0];
-  uint32_t zl[32];
-  q.zor = slow_block(row, cnt, a.qp, zl, &q.flags);
-  store_codes(zs, lane, q.x0, zl);
-  if ((q.flags & 4) && S.report_base != NO_REPORT) {
-    const float* src = S.x + v0 + (uint64_t)lane * 32;
-    for (int j = 0; j < cnt; ++j)
-      if (!isfinite(SRC == SRC_STEP ? src[j] : row[j])) {
-        atomicMin(&a.st->first_nonfinite, (unsigned long long)(S.report_base + v0 + (uint64_t)lane * 32 + j));
-        break;
-      }
-  }
-}
-
-// Phase A for one warp tile (values in xs): quantise and pack the tile into
-// `dst` (its scratch or output slot).
-template <int SRC, int NSEG, bool FAST>
-__device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg& S, const SegGeom& G, uint64_t tile,
-                                           float* xs, uint32_t* dst, uint32_t* stage, int in_base, int in_bytes,
-                                           int in_w, const double* s_step, uint64_t pol_keep, int lane) {
-  const uint64_t nb = G.nb, b0 = tile * TB, v0 = b0 * BLOCK;
-  const int last_cnt = G.last_cnt;
-  const int nblk = (int)(nb - b0 < (uint64_t)TB ? nb - b0 : (uint64_t)TB);
-  const int nval = (int)(G.n - v0 < (uint64_t)TILE_VALUES ? G.n - v0 : (uint64_t)TILE_VALUES);
-  int base = 0, in_start = -1;
-
-  // ---- 1. fused step: combine the received blob's tile into xs
-  // (its compressed bytes were staged asynchronously with the local values)
-  if (SRC == SRC_STEP) {
-    base = in_base;
-    in_start = block_start(stage, base, in_bytes, in_w, nblk, b0, nb, last_cnt, a.st, lane);
-    __syncwarp();
-    decode_row<1>(stage, base, in_start, in_w, b0, nb, last_cnt, a.in_tw, xs, a.op, s_step, lane);
-    __syncwarp();
-    if (a.acc_out) drain_values(xs, a.acc_out, v0, nval, lane);
-    __syncwarp();
-  }
-
-  // ---- 2. closed-loop quantisation, one lane per 32-value block; the codes
-  // replace the values in the lane's shared-memory row -- except in the fused
-  // step, whose consumed staging buffer takes them, so that the rare raw or
-  // unproven block still finds its values (local + received) in xs
-  __syncwarp();
-  float* zs = SRC == SRC_STEP ? reinterpret_cast<float*>(stage) : xs;
-  const bool active = lane < nblk;
-  const int cnt = active ? ((b0 + lane == nb - 1) ? last_cnt : 32) : 0;
-  QOut q{0u, 0, 0.0f};
-  if (active) {
-    int fb = FB_SLOW;
-    if (FAST && cnt == 32) fb = fast_block(xs, zs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, q.zor, q.x0);
-    if (fb == FB_SLOW)  // rare: exact replay of the whole block
-      slow_replay<SRC, NSEG>(a, S, v0, cnt, xs, FAST && cnt == 32 && zs == xs, zs, q, stage, base, in_start, in_w,
-                             s_step, lane);
-    else if (fb == FB_RAW)
-      q.flags |= 2;
-  }
-  return pack_tile<SRC, NSEG>(a, S, G, tile, xs, zs, dst, q, stage, base, in_start, in_w, s_step, pol_keep, lane);
 }
 
 // Encoder, kernel 1 of 2 (one CTA per SM, no CTA-wide barrier after setup).
@@ -672,6 +647,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   InMeta m_cur = ONEBUF ? load_meta(j) : InMeta{0, 0, 0};
   if (j < total && !ONEBUF) prefetch_tile(a, j, xsb0, lane, pol_in);
   int buf = 0;
+  uint32_t dummy = 0;
   while (j < total) {
     InMeta m_nxt{0, 0, 0};
     if (ONEBUF) {
@@ -693,8 +669,9 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     const SegGeom G = seg_geom(S.n);
     const uint64_t t = j - S.tile_base;
     const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
-                                                reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), stg0,
-                                                in_cur.base, in_cur.bytes, in_cur.w, s_step, pol_keep, lane);
+                                                reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), 0,
+                                                false, dummy, stg0, in_cur.base, in_cur.bytes, in_cur.w, s_step,
+                                                pol_keep, lane);
     if (lane == 0) {
       a.tile_rel[j] = (uint32_t)tb;
       if (!a.slotted_out) {
