@@ -69,6 +69,10 @@ struct EncodeArgs {
 // buffer per warp): 24 warps per SM hide the latency better than 16
 // double-buffered or 13 fully asynchronous warps (measured, profiles/).
 constexpr int ENC_WARP_SMEM = TILE_VALUES * 4 + STAGE_BYTES;
+#ifndef GZ_STEP_L2PF
+#define GZ_STEP_L2PF 1
+#endif
+constexpr bool L2PF = GZ_STEP_L2PF;  // fused step: L2 prefetch of the next tile
 // warps per encoder CTA (one CTA per SM): as many as shared memory allows
 __host__ __device__ constexpr int enc_warps(int src) { return 24; }
 
@@ -443,7 +447,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   float x0 = 0.0f;
   if (active) {
     int fb = FB_SLOW;
-    if (FAST && cnt == 32) fb = fast_block(xs, zs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
+    if (FAST && cnt == 32) fb = fast_block<SRC == SRC_STEP>(xs, zs, lane, a.qp.tw, a.qp.rtw, a.qp.thr, a.qp.elo, a.qp.ehi, zor, x0);
     if (fb == FB_SLOW) {  // rare: exact replay of the whole block
       float row[32];
       if (FAST && cnt == 32 && zs == xs) reload_row<SRC>(a, S, v0, cnt, stage, base, a.in_tw, s_step, in_start, in_w, lane, row);
@@ -622,8 +626,10 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   // fused step, one buffer: the received tile's sidecar entries (offsets,
   // widths) are loaded one tile ahead; its bytes and the local values are
   // fetched together (one cp.async group) when the tile starts
+  // (the loads stay in flight until the tile starts: nothing here consumes
+  // them -- with slotted input they are NVLink reads of the peer's sizes)
   struct InMeta {
-    uint64_t ts, te;
+    uint64_t ts, te;  // slotted input: te holds the tile's size until the tile starts
     int w;
   };
   auto load_meta = [&](unsigned int jn) {
@@ -631,7 +637,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     if (SRC == SRC_STEP && jn < total) {
       if (a.in_slots) {  // slotted input: the tile sits at the start of its slot
         m.ts = (uint64_t)jn * TILE_SLOT;
-        m.te = m.ts + a.in_sizes[jn];
+        m.te = a.in_sizes[jn];
       } else {
         m.ts = a.in_tile_off[jn];
         m.te = a.in_tile_off[jn + 1];
@@ -639,6 +645,9 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
       m.w = a.in_w[(uint64_t)jn * TB + lane];
     }
     return m;
+  };
+  auto meta_end = [&](InMeta& m) {
+    if (a.in_slots) m.te += m.ts;
   };
   const uint8_t* const in_base = a.in_slots ? a.in_slots : a.in_blob + HEADER_BYTES;
   unsigned int j = s_abort ? total : claim();
@@ -652,6 +661,16 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     InMeta m_nxt{0, 0, 0};
     if (ONEBUF) {
       m_nxt = load_meta(j1);
+      // warm L2 with the next tile's local values (4 KB) and the first 1 KB of
+      // its received slot (most tiles): their cp.async at the next tile's
+      // start then waits on L2, not on HBM / NVLink
+      if (L2PF && j1 < total) {
+        const int k1 = NSEG > 1 ? seg_of_tile(a, j1) : 0;
+        const uint64_t v1 = (uint64_t)(j1 - a.seg[k1].tile_base) * TILE_VALUES;
+        if (v1 + (uint64_t)lane * 32 < a.seg[k1].n)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(a.seg[k1].x + v1 + lane * 32));
+      }
+      meta_end(m_cur);
       if (m_cur.te < m_cur.ts || m_cur.te - m_cur.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m_cur.te = m_cur.ts;  // corrupt sidecar
       in_cur.base = stage_bytes<true>(stg0, in_base, m_cur.ts, m_cur.te, lane);
       in_cur.bytes = (int)(m_cur.te - m_cur.ts);

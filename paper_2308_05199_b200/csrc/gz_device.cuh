@@ -203,6 +203,9 @@ __device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, c
 //   maximum inside [elo, ehi] is undecided.
 enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
 
+// COMPACT: the seven 4-step chunks after the first run as a loop (a quarter
+// of the code; for kernels whose hot loop would not fit the instruction cache).
+template <bool COMPACT = false>
 __device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, double tw, float rtw, float thr,
                                           float elo, float ehi, uint32_t& zor_out, float& x0) {
   // The codes go to the same row of zs (zs == xs: they overwrite the
@@ -215,12 +218,7 @@ __device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, d
   float frmax = 0.0f;  // max |vf - q|
   float emax = 0.0f;   // max |rec - x|
   uint32_t zor = 0;
-  uint32_t zc[4];
-  zc[0] = __float_as_uint(x0);
-#pragma unroll
-  for (int j = 1; j < 32; ++j) {
-    if ((j & 3) == 0) c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, j >> 2));
-    const float x = (j & 3) == 0 ? c4.x : (j & 3) == 1 ? c4.y : (j & 3) == 2 ? c4.z : c4.w;
+  auto step = [&](float x) -> uint32_t {
     const float vf = __fmul_rn(__fsub_rn(x, prev32), rtw);
     const float m = __fadd_rn(vf, MAGIC32);
     frmax = fmaxf(frmax, fabsf(__fsub_rn(vf, __fsub_rn(m, MAGIC32))));
@@ -235,9 +233,17 @@ __device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, d
     asm("{\n\t.reg .b32 s, d;\n\tshr.s32 s, %1, 31;\n\tadd.u32 d, %1, %1;\n\tlop3.b32 %0, d, s, 0, 0xC3;\n\t}"
         : "=r"(z) : "r"(qb));
     zor |= z;
-    zc[j & 3] = z;
-    if ((j & 3) == 3)
-      *reinterpret_cast<uint4*>(zs + xs_index(row, j >> 2)) = make_uint4(zc[0], zc[1], zc[2], zc[3]);
+    return z;
+  };
+  {
+    const uint32_t z1 = step(c4.y), z2 = step(c4.z), z3 = step(c4.w);
+    *reinterpret_cast<uint4*>(zs + xs_index(row, 0)) = make_uint4(__float_as_uint(x0), z1, z2, z3);
+  }
+#pragma unroll(COMPACT ? 1 : 7)
+  for (int c = 1; c < 8; ++c) {
+    c4 = *reinterpret_cast<const float4*>(xs + xs_index(row, c));
+    const uint32_t z0 = step(c4.x), z1 = step(c4.y), z2 = step(c4.z), z3 = step(c4.w);
+    *reinterpret_cast<uint4*>(zs + xs_index(row, c)) = make_uint4(z0, z1, z2, z3);
   }
   zor_out = zor;
   const int w = 32 - __clz(zor);
