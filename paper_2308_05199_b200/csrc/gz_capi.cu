@@ -124,7 +124,7 @@ WsView carve(void* ws, uint64_t tiles) {
 template <int SRC, int NSEG, bool FAST>
 int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   constexpr int NW = enc_warps(SRC);
-  const size_t smem = (size_t)NW * (SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4);
+  const size_t smem = (size_t)NW * enc_warp_smem(SRC);
   static int caps[MAXDEV];
   const int cap = grid_cap(k_tile_encode<SRC, NSEG, FAST>, 32 * NW, smem, caps);
   // one CTA per tile up to one per SM: a small message is spread over as many

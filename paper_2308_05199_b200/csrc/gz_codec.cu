@@ -74,7 +74,9 @@ constexpr int ENC_WARP_SMEM = TILE_VALUES * 4 + STAGE_BYTES;
 #endif
 constexpr bool L2PF = GZ_STEP_L2PF;  // fused step: L2 prefetch of the next tile
 // warps per encoder CTA (one CTA per SM): as many as shared memory allows
+// (18 warps with double-buffered local values: 2^25 peer step 114 -> 121 us)
 __host__ __device__ constexpr int enc_warps(int src) { return 24; }
+__host__ __device__ constexpr int enc_warp_smem(int src) { return src == 1 ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4; }
 
 // -------------------------------------------------------------------------
 // small helpers
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   // this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int WSMEM = SRC == SRC_STEP ? ENC_WARP_SMEM : 2 * TILE_VALUES * 4;
+  constexpr int WSMEM = enc_warp_smem(SRC);
   unsigned char* my = smem + warp * WSMEM;
   float* xsb0 = reinterpret_cast<float*>(my);
   constexpr bool ONEBUF = SRC == SRC_STEP;  // the fused step: one value buffer + one staging buffer
