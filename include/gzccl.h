@@ -215,6 +215,12 @@ int gz_copy_checked(const float* src, float* dst, uint64_t n, uint64_t report_ba
 /* out[n] = op(local, recv): _apply_op (collectives.py:32-39), op 0 = sum (binary32
  * RN), 1 = np.maximum (NaN propagates, ties return recv).  out may alias local. */
 int gz_apply_op(const float* local, const float* recv, float* out, uint64_t n, int op, gz_stream_t stream);
+/* key[i] = status word i (first_nonfinite, decode_error, trailing, comm_error)
+ * as (rank << 56) | value, or INT64_MAX where it holds no error: a MIN
+ * all-reduce of the keys over the ranks gives, per word, the lowest rank that
+ * recorded an error and its value (the rank-ordered raise of
+ * collectives.py:202-205).  rank < 128. */
+int gz_status_key(const gz_status* d_status, int rank, int64_t* d_key, gz_stream_t stream);
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream);
 /* the same on at most sms_budget SMs (0: all), so that it can run beside a
  * decoder launched with reserve_sms = sms_budget (allgather pipeline) */

@@ -50,6 +50,7 @@ SIGNATURES = {
     "gz_copy_items": (i32, [p, u32, p]),
     "gz_copy_checked": (i32, [p, p, u64, u64, p, p]),
     "gz_apply_op": (i32, [p, p, p, u64, i32, p]),
+    "gz_status_key": (i32, [p, i32, p, p]),
     "gz_copy_items_sms": (i32, [p, u32, i32, p]),
     "gz_launch_count": (u64, []),
     "gz_debug_stamp": (i32, [p, p]),

@@ -43,6 +43,8 @@ from .schedule import Compress, Reduce, ring_allreduce_plan
 _ALIGN = 256
 _MAX_DECODE_SEGMENTS = 8  # GZ_MAX_DECODE_SEGMENTS (include/gzccl.h)
 _NO_REPORT = (1 << 64) - 1  # gz_step_io.report_base: `local` is not the caller's input
+_KEY_NONE = (1 << 63) - 1  # check(): no error on any rank
+_KEY_MASK = (1 << 56) - 1
 AG_COPY_SMS = 24  # SMs left to the allgather's NVLink pulls while the previous owner's blob is decoded
 AG_MULTI_MAX = 8 << 20  # chunk values up to which the allgather decodes every owner in one remote-read launch
 
@@ -393,14 +395,17 @@ class Communicator:
         ev = torch.cuda.Event()
         ev.record(torch.cuda.current_stream(self.device))
         t0 = time.perf_counter()
-        delay = 1e-5
+        # spin for the first 2 ms (a collective usually ends within that:
+        # sleeping would add the scheduler's wake-up latency to every call),
+        # then back off
         while not ev.query():
-            if time.perf_counter() - t0 > self.flag_timeout_s:
+            waited = time.perf_counter() - t0
+            if waited > self.flag_timeout_s:
                 self._poison()
                 raise TimeoutError(f"rank {self.rank}: {what} did not complete within {self.flag_timeout_s} s "
                                    "(a peer never posted its flag); the communicator is unusable")
-            time.sleep(delay)
-            delay = min(delay * 2, 1e-2)
+            if waited > 2e-3:
+                time.sleep(min(1e-2, waited / 8))
 
     def _poison(self):
         side = torch.cuda.Stream(self.device)
@@ -414,28 +419,33 @@ class Communicator:
     def check(self):
         """Wait for the outstanding calls of this rank (bounded) and raise the
         first error any rank's kernels recorded since the last reset, on every
-        rank alike (the reference raises for the whole collective)."""
-        import numpy as np
-
-        from .codec import DecodeError, _NONE
+        rank alike (the reference raises for the whole collective).  The ranks'
+        status words are combined on the device (one MIN all-reduce of
+        (rank << 56 | value) keys, so the lowest rank with an error wins, as in
+        collectives.py:202-205), then read with one small copy."""
+        from .codec import DecodeError
 
         if getattr(self, "_broken", False):
             raise RuntimeError("communicator is unusable after a peer timeout")
+        if not hasattr(self, "_st_key"):
+            self._st_key = torch.empty(4, dtype=torch.int64, device=self.device)
+        key = self._st_key
+        L.check(L.lib().gz_status_key(self.ws.status_ptr(), self.rank, key.data_ptr(),
+                                      torch.cuda.current_stream(self.device).cuda_stream), "gz_status_key")
+        if self.world > 1:
+            dist.all_reduce(key, op=dist.ReduceOp.MIN, group=self.group)
+        if not hasattr(self, "_st_host"):
+            self._st_host = torch.empty(4, dtype=torch.int64, pin_memory=True)
+        self._st_host.copy_(key, non_blocking=True)
         self._bounded_sync()
-        st = self.ws.status[:4].cpu().numpy().view(np.uint64)
-        mine = [int(v) for v in st]
-        alls = [None] * self.world
-        dist.all_gather_object(alls, mine, group=self.group)
-        for r, v in enumerate(alls):
-            if v[3] != _NONE:
-                raise RuntimeError(f"rank {r}: a peer flag never arrived (in-kernel wait gave up after 20 s)")
-        for r, v in enumerate(alls):  # collectives.py:202-205: the first bad buffer in rank order
-            if v[0] != _NONE:
-                raise ValueError(f"non-finite value at offset {v[0]}")
-        for r, v in enumerate(alls):
-            if v[1] != _NONE:
-                e = v[1]
-                raise DecodeError(f"rank {r}: inconsistent compressed stream at block {e >> 24} (code {e & 0xFF})")
+        k = [int(v) for v in self._st_host.tolist()]
+        if k[3] != _KEY_NONE:
+            raise RuntimeError(f"rank {k[3] >> 56}: a peer flag never arrived (in-kernel wait gave up after 20 s)")
+        if k[0] != _KEY_NONE:
+            raise ValueError(f"non-finite value at offset {k[0] & _KEY_MASK}")
+        if k[1] != _KEY_NONE:
+            e = k[1] & _KEY_MASK
+            raise DecodeError(f"rank {k[1] >> 56}: inconsistent compressed stream at block {e >> 24} (code {e & 0xFF})")
 
     def _check_input(self, x):
         if not isinstance(x, torch.Tensor) or x.dim() != 1 or x.dtype != torch.float32 or not x.is_cuda:

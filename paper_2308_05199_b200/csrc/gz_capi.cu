@@ -832,6 +832,19 @@ int gz_apply_op(const float* local, const float* recv, float* out, uint64_t n, i
   return (int)cudaGetLastError();
 }
 
+__global__ void k_status_key(const unsigned long long* st, long long rank, long long* key) {
+  const int i = threadIdx.x;
+  if (i < 4) key[i] = st[i] == ~0ull ? 0x7FFFFFFFFFFFFFFFll : (long long)(st[i] | ((unsigned long long)rank << 56));
+}
+
+int gz_status_key(const gz_status* d_status, int rank, int64_t* d_key, gz_stream_t stream) {
+  if (!d_status || !d_key || rank < 0 || rank >= 128) return GZ_EINVAL;
+  count_launch();
+  k_status_key<<<1, 32, 0, (cudaStream_t)stream>>>(reinterpret_cast<const unsigned long long*>(d_status), rank,
+                                                   reinterpret_cast<long long*>(d_key));
+  return (int)cudaGetLastError();
+}
+
 int gz_copy_items(const gz_copy_item* items, uint32_t count, gz_stream_t stream) {
   return gz_copy_items_sms(items, count, 0, stream);
 }
