@@ -977,9 +977,9 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     if (t < total) {
       const DecSeg& S = a.seg[seg_of(t)];
       const uint64_t lt = t - S.tile_base;
-      if (S.sizes) {
+      if (S.sizes) {  // te holds the size until stage() (a peer read: nothing consumes it yet)
         m.ts = lt * TILE_SLOT;
-        m.te = m.ts + S.sizes[lt];
+        m.te = S.sizes[lt];
       } else {
         m.ts = S.tile_off[lt];
         m.te = S.tile_off[lt + 1];
@@ -993,6 +993,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     w = 0;
     if (t < total) {
       const DecSeg& S = a.seg[seg_of(t)];
+      if (S.sizes) m.te += m.ts;
       // a corrupt sidecar must not overflow the staging buffer: stage nothing,
       // block_start() then reports the mismatch (checked here, where the offsets
       // are consumed, so their loads stay in flight behind the previous tile)
