@@ -470,7 +470,17 @@ int gz_decompress_slots_multi(const uint8_t* const* slots, const uint32_t* const
   a.total_tiles = tiles;
   a.tw = 2.0 * eb;
   a.st = reinterpret_cast<Status*>(d_status);
-  // the slots are usually in peer GPUs' memory: the three-stage (two tiles ahead) decoder
+  if (k == 1) {  // a single owner: the two-stage decoder (2^26 peer slots: 109 -> 97 us)
+    DecodeMultiArgs<1> b;
+    std::memset(&b, 0, sizeof(b));
+    b.seg[0] = a.seg[0];
+    b.nseg = 1;
+    b.total_tiles = tiles;
+    b.tw = a.tw;
+    b.st = a.st;
+    return launch_decode<1>(b, (cudaStream_t)stream, reserve_sms);
+  }
+  // several owners (usually in peer GPUs' memory) in one launch
   return launch_decode<GZ_MAX_DECODE_SEGMENTS>(a, (cudaStream_t)stream, reserve_sms);
 }
 

@@ -942,10 +942,10 @@ struct DecodeMultiArgs {
   uint64_t report_base;    // offset of local[0] in the caller's buffer (first_nonfinite reports)
 };
 
-// Stages per warp: 2 (one tile ahead) for local blobs; 3 (two tiles ahead)
-// when decoding several blobs out of peer GPUs' memory, where the NVLink
-// latency needs more bytes in flight.
-__host__ __device__ constexpr int dec_stages(int nseg) { return nseg > 1 ? 3 : 2; }
+// Stages per warp: 2 (one tile ahead), also for peer memory
+// (three stages for the multi-owner allgather measured 3 % slower at N = 4 once
+// the slotted sizes stay in flight, fewer resident warps)
+__host__ __device__ constexpr int dec_stages(int nseg) { return 2; }
 __host__ __device__ constexpr int dec_warp_smem(int nseg) { return TILE_VALUES * 4 + dec_stages(nseg) * STAGE_BYTES; }
 
 template <int NSEG>
