@@ -86,12 +86,23 @@ inline int dev_sms(int dev) {
 
 // Persistent grid: as many CTAs as fit on the device at once (per device),
 // after opting the kernel into `smem` bytes of dynamic shared memory there.
+#ifndef GZ_FUSED_GATHER
+#define GZ_FUSED_GATHER 0
+#endif
+#ifndef GZ_CARVEOUT_MAX
+#define GZ_CARVEOUT_MAX 0
+#endif
 template <typename K>
 int grid_cap(K kernel, int threads, size_t smem, int (&cache)[MAXDEV]) {
   const int dev = cur_dev();
   if (cache[dev] == 0) {
     int occ = 0;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+#if GZ_CARVEOUT_MAX
+    // every kernel of the library asks for the same L1/shared split, so consecutive
+    // launches (encoder -> gather -> decoder) never wait for an SM to be reconfigured
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     cache[dev] = (occ > 0 ? occ : 1) * dev_sms(dev) + 1;
   }
@@ -145,7 +156,10 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   // tiles per gather group (one warp each): 8, doubled until the groups fit
   // MAXGRID; halved (down to 1) while there are fewer groups than ~8 warps
   // per SM -- a small message's gather is a per-warp latency chain
-  uint32_t gs = 3;
+#ifndef GZ_GATHER_GS
+#define GZ_GATHER_GS 3
+#endif
+  uint32_t gs = GZ_GATHER_GS;
   auto ngroups = [&](uint32_t sh) {
     uint64_t g = 0;
     for (int k = 0; k < a.nseg; ++k) g += std::max<uint64_t>(1, (ntiles_of(a.seg[k].n) + (1u << sh) - 1) >> sh);
@@ -163,26 +177,35 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   a.gshift = gs;
   a.ngctas = gbase;
   count_launch();
+  if (GZ_FUSED_GATHER && !a.slotted_out) {
+    // one cooperative launch: the encoder grid gathers its own blob after a
+    // grid barrier (all CTAs resident: one per SM)
+    a.fused_gather = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)base);
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k_tile_encode<SRC, NSEG, FAST>, a);
+  }
+  a.fused_gather = 0;
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   int rc = (int)cudaGetLastError();
   if (rc) return rc;
   if (a.slotted_out) return 0;  // slotted output: the consumer reads the slots
   count_launch();
-  // gather: programmatic dependent launch, so its CTAs start as encoder CTAs retire
+  // gather: a plain stream-ordered launch (a programmatic dependent launch measured
+  // 5-6 us slower per call at cfg1: 50.2 -> 44.0 us, tools/exp/ab_codec2.py)
   static int gcaps[MAXDEV];
   const int gcap = grid_cap(k_gather<NSEG>, GATHER_THREADS, 0, gcaps);
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)std::min<uint64_t>((gbase + GATHER_THREADS / 32 - 1) / (GATHER_THREADS / 32),
-                                                  (uint64_t)gcap));
-  cfg.blockDim = dim3(GATHER_THREADS);
-  cfg.dynamicSmemBytes = 0;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, k_gather<NSEG>, a);
+  const unsigned ggrid = (unsigned)std::min<uint64_t>((gbase + GATHER_THREADS / 32 - 1) / (GATHER_THREADS / 32), (uint64_t)gcap);
+  k_gather<NSEG><<<ggrid, GATHER_THREADS, 0, s>>>(a);
+  return (int)cudaGetLastError();
 }
 
 template <int SRC, int NSEG>

@@ -60,7 +60,13 @@ struct EncodeArgs {
   int slotted_out;         // 1: the output stays in slotted form (scratch/tile_rel), no gather
   unsigned int* post_flag; // slotted only, may be null: set to 1 once the whole output is written
   unsigned int* wait_flag; // slotted only, may be null: wait until >= 1 before reading inputs, reset to 0
+  int fused_gather;        // 1: the encoder grid (a cooperative launch) gathers the blob itself after a grid barrier
 };
+
+template <int NSEG>
+__device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_t gw, uint64_t nwarps, int lane);
+template <int NSEG>
+__device__ __forceinline__ void gather_retire(const EncodeArgs<NSEG>& a, int* s_last);
 
 
 
@@ -515,6 +521,9 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
         load_codes(zs, lane, z);
         if (w <= 8) {
           const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
+          // the codes carry ZBIAS: every quad of 4 codes carries ZBIAS (1 + P1)(1 + P2)
+          // modulo 2^32 (code 31 is a biased zero), removed once per quad
+          const uint32_t K = ZBIAS * (1u + P1) * (1u + P2);
           const int CB = (ncodes * w + 7) >> 3;
 #pragma unroll
           for (int g = 0; g < 4; ++g) {
@@ -522,9 +531,9 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const int j0 = 8 * g + 2 * i;
-              pr[i] = (j0 + 1 < 31) ? z[j0] + z[j0 + 1] * P1 : z[j0];
+              pr[i] = z[j0] + ((j0 + 1 < 31) ? z[j0 + 1] : ZBIAS) * P1;
             }
-            const uint32_t qa = pr[0] + pr[1] * P2, qb2 = pr[2] + pr[3] * P2;
+            const uint32_t qa = pr[0] + pr[1] * P2 - K, qb2 = pr[2] + pr[3] * P2 - K;
             const uint64_t oct = (uint64_t)qa | ((uint64_t)qb2 << (4 * w));
             const int L = min(w, CB - g * w);
             if (L > 0) ap.append(oct, L);
@@ -535,7 +544,7 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
 #pragma unroll
           for (int j = 0; j < 31; ++j) {
             if (j < ncodes) {
-              acc |= (uint64_t)z[j] << nbits;
+              acc |= (uint64_t)(z[j] - ZBIAS) << nbits;
               nbits += w;
               if (nbits >= 32) {
                 ap.append(acc & 0xFFFFFFFFull, 4);
@@ -575,9 +584,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
   __shared__ unsigned int s_next;
   __shared__ int s_abort;
-  // the gather kernel may be scheduled as soon as SMs free up; it waits for
-  // this grid's completion itself (griddepcontrol.wait)
-  asm volatile("griddepcontrol.launch_dependents;");
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   constexpr int WSMEM = enc_warp_smem(SRC);
   unsigned char* my = smem + warp * WSMEM;
@@ -688,18 +694,20 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     const int k = NSEG > 1 ? seg_of_tile(a, j) : 0;
     const Seg& S = a.seg[k];
     const SegGeom G = seg_geom(S.n);
-    const uint64_t t = j - S.tile_base;
+    const uint64_t t = NSEG > 1 ? j - S.tile_base : j;  // one segment: tile_base == 0
     const int tb = encode_tile<SRC, NSEG, FAST>(a, S, G, t, buf ? xsb1 : xsb0,
                                                 reinterpret_cast<uint32_t*>(a.scratch + (uint64_t)j * TILE_SLOT), 0,
                                                 false, dummy, stg0, in_cur.base, in_cur.bytes, in_cur.w, s_step,
                                                 pol_keep, lane);
-    if (lane == 0) {
-      a.tile_rel[j] = (uint32_t)tb;
-      if (!a.slotted_out) {
-        const uint64_t g = S.gcta_base + (t >> a.gshift);
-        atomicAdd(&a.ws->agg[g], (unsigned)tb);
-        atomicAdd(&a.ws->agg2[g >> 5], (unsigned)tb);
-        atomicAdd(&a.ws->agg3[g >> 10], (unsigned)tb);
+    // the tile's size and the three counter updates (agg, agg2, agg3 are
+    // consecutive arrays of TileWs), one lane each
+    if (lane < 4) {
+      if (lane == 3) {
+        a.tile_rel[j] = (uint32_t)tb;
+      } else if (!a.slotted_out) {
+        const uint32_t g = (uint32_t)((NSEG > 1 ? S.gcta_base : 0) + (t >> a.gshift));
+        const uint32_t idx = lane == 0 ? g : lane == 1 ? MAXGRID + (g >> 5) : MAXGRID + MAXGRID / 32 + (g >> 10);
+        atomicAdd(a.ws->agg + idx, (unsigned)tb);
       }
     }
     __syncwarp();
@@ -709,6 +717,29 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
+  if (a.fused_gather) {
+    // grid barrier (every CTA is resident: cooperative launch, one CTA per SM):
+    // warps that ran out of tiles wait at the CTA barrier, so they take no
+    // issue slots from the CTA's encoding warps; one thread per CTA spins
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      atomicAdd(&a.ws->arrive, 1u);
+      unsigned int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&a.ws->arrive) : "memory");
+        if (v >= gridDim.x) break;
+        __nanosleep(64);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+    gather_groups(a, (uint64_t)blockIdx.x * NW + warp, (uint64_t)gridDim.x * NW, lane);
+    gather_retire(a, &s_last);
+    return;
+  }
   if (a.slotted_out) {
     // no gather kernel follows: the last CTA re-zeroes the claim counter and
     // posts the step's completion flag (a peer's, over NVLink) itself, so a
@@ -740,10 +771,15 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
 // moves its tiles as aligned 16-byte chunks into the blob -- possibly in a
 // peer GPU's memory (the NVLink send of a fused reduce-scatter step).  The
 // first batch of slot windows is loaded together with the sizes and
-// counters.  Launched as a programmatic dependent of the encoder, so its
-// launch overlaps the encoder's tail.
+// counters.  A plain stream-ordered launch after the encoder.
 constexpr int GATHER_THREADS = 256;
-constexpr int GATHER_U = 4;  // tiles per batch
+#ifndef GZ_GATHER_U
+#define GZ_GATHER_U 4
+#endif
+#ifndef GZ_GATHER_MINB
+#define GZ_GATHER_MINB 1
+#endif
+constexpr int GATHER_U = GZ_GATHER_U;  // tiles per batch
 
 // Copy one tile (L bytes at a 128-aligned slot) to dst (any alignment) with
 // the whole warp; `cur` holds slot chunk `lane` (prefetched), hb/tb the
@@ -784,16 +820,13 @@ __device__ __forceinline__ void gather_tile(uint8_t* dst, const uint8_t* src, in
   if (lane >= 16 && lane - 16 < L - t0) dst[t0 + lane - 16] = (uint8_t)tb;
 }
 
+// The gather groups of warp `gw` of `nwarps` (warp-strided).
 template <int NSEG>
-__global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG> a) {
+__device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_t gw, uint64_t nwarps, int lane) {
   constexpr int U = GATHER_U;
-  __shared__ int s_last;
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // the encoder grid is complete
-  const int tid = threadIdx.x, lane = tid & 31;
   TileWs* ws = a.ws;
-  const uint64_t nwarps = (uint64_t)gridDim.x * (GATHER_THREADS / 32);
   const uint64_t cend = a.ngctas;
-  for (uint64_t c = (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (tid >> 5); c < cend; c += nwarps) {
+  for (uint64_t c = gw; c < cend; c += nwarps) {
     int k = 0;
     if (NSEG > 1) {
 #pragma unroll 1
@@ -901,19 +934,35 @@ __global__ void __launch_bounds__(GATHER_THREADS) k_gather(const EncodeArgs<NSEG
       *S.out_len = HEADER_BYTES + base;
     }
   }
-  // ---- retire: the last CTA zeroes the counters for the next launch
+}
+
+// Retire (every thread of the CTA): the last CTA to get here zeroes the
+// counters (and the grid barrier word) for the next launch.
+template <int NSEG>
+__device__ __forceinline__ void gather_retire(const EncodeArgs<NSEG>& a, int* s_last) {
+  TileWs* ws = a.ws;
+  const int tid = threadIdx.x, nt = blockDim.x;
   __syncthreads();
-  if (tid == 0) s_last = atomicAdd(&ws->done, 1ull) == gridDim.x - 1;
+  if (tid == 0) *s_last = atomicAdd(&ws->done, 1ull) == gridDim.x - 1;
   __syncthreads();
-  if (s_last) {
-    for (uint64_t g = tid; g < a.ngctas; g += GATHER_THREADS) ws->agg[g] = 0;
-    for (uint64_t g = tid; g < (a.ngctas + 31) / 32; g += GATHER_THREADS) ws->agg2[g] = 0;
-    for (uint64_t g = tid; g < (a.ngctas + 1023) / 1024; g += GATHER_THREADS) ws->agg3[g] = 0;
+  if (*s_last) {
+    for (uint64_t g = tid; g < a.ngctas; g += nt) ws->agg[g] = 0;
+    for (uint64_t g = tid; g < (a.ngctas + 31) / 32; g += nt) ws->agg2[g] = 0;
+    for (uint64_t g = tid; g < (a.ngctas + 1023) / 1024; g += nt) ws->agg3[g] = 0;
     if (tid == 0) {
       ws->done = 0;
       ws->claim = 0;
+      ws->arrive = 0;
     }
   }
+}
+
+template <int NSEG>
+__global__ void __launch_bounds__(GATHER_THREADS, GZ_GATHER_MINB) k_gather(const EncodeArgs<NSEG> a) {
+  __shared__ int s_last;
+  gather_groups(a, (uint64_t)blockIdx.x * (GATHER_THREADS / 32) + (threadIdx.x >> 5),
+                (uint64_t)gridDim.x * (GATHER_THREADS / 32), threadIdx.x & 31);
+  gather_retire(a, &s_last);
 }
 
 // -------------------------------------------------------------------------

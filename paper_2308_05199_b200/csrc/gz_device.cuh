@@ -27,6 +27,7 @@
 // ufunc of the reference; see fast_block() for the exactness argument
 // behind the f32 fast path.
 #pragma once
+#include <cstddef>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -46,6 +47,13 @@ constexpr int STAGE_BYTES = TB * MAX_BLOCK_BYTES + 64;     // packed tile + slac
 constexpr int STAGE_WORDS = STAGE_BYTES / 4;
 constexpr float MAGIC32 = 12582912.0f;                     // 1.5 * 2^23
 constexpr int MAGIC32_BITS = 0x4B400000;
+constexpr double M52_PLUS_MAGIC32 = 4503599627370496.0 + (double)MAGIC32_BITS;  // 2^52 + bits(MAGIC32)
+// zigzag codes in shared memory carry the bias ZBIAS = bits(2^23) (fast_block forms
+// them as the binary32 2^23 + z); the bias is removed modulo 2^32 when packing
+constexpr uint32_t ZBIAS = 0x4B000000u;
+constexpr uint32_t ZBIAS_MASK = 0x001FFFFFu;
+// every biased code of a block is ZBIAS + z with z < 2^21
+__device__ __forceinline__ bool zbias_valid(uint32_t zor) { return (zor & ~ZBIAS_MASK) == ZBIAS; }
 
 // ---- device workspace: zero-initialised once, reused by every launch -------
 // Layout: this header, tile sizes (u32 per tile), scratch slots.
@@ -61,10 +69,16 @@ struct TileWs {
   unsigned long long pad0[15];
   unsigned int claim;               // encoder tile claims (own 128-byte line)
   unsigned int pad1[31];
+  unsigned int arrive;              // grid barrier of the fused encoder + gather (own 128-byte line)
+  unsigned int pad2[31];
   unsigned int agg[MAXGRID];
   unsigned int agg2[MAXGRID / 32];
   unsigned int agg3[MAXGRID / 1024];
 };
+// the encoder addresses agg2 / agg3 as agg[MAXGRID + ...]
+static_assert(offsetof(TileWs, agg2) == offsetof(TileWs, agg) + 4 * MAXGRID &&
+                  offsetof(TileWs, agg3) == offsetof(TileWs, agg2) + 4 * (MAXGRID / 32),
+              "TileWs counter arrays must be consecutive");
 
 struct Status {                          // error reporting (host-reset to ~0)
   unsigned long long first_nonfinite;    // codec.py:83-85
@@ -201,6 +215,14 @@ __device__ __noinline__ uint32_t slow_block(const float* xs_row_vals, int cnt, c
 //   max e < elo (<= eb (1 - 2^-22)) proves every |rec - x| <= eb and
 //   max e > ehi (>= eb (1 + 2^-22)) proves some |rec - x| > eb; only a
 //   maximum inside [elo, ehi] is undecided.
+//   The zigzag code is formed in binary32 as well: with q exact, tz = 2q + 1/2 is exact
+//   and RN32(|tz| + (2^23 - 1/2)) = 2^23 + z exactly (z = |2q + 1/2| - 1/2 = zigzag(q)),
+//   so its bits are ZBIAS + z.  The codes are kept in this biased form in shared
+//   memory (packing removes the bias with modular arithmetic).  If |vf| >= 2^22 (m
+//   outside the magic range), or vf is Inf/NaN, |tz| >= 2^23 - 1/2 or is Inf/NaN, so
+//   the biased code has bits 21..23 set or an exponent other than 150: requiring the
+//   OR of the biased codes to equal ZBIAS in bits 21..31 proves every z < 2^21 (the
+//   former w <= 21 test, now also covering the range of m).
 enum { FB_PACKED = 0, FB_RAW = 1, FB_SLOW = 2 };
 
 // COMPACT: the seven 4-step chunks after the first run as a loop (a quarter
@@ -217,21 +239,22 @@ __device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, d
   double prev64 = (double)prev32;
   float frmax = 0.0f;  // max |vf - q|
   float emax = 0.0f;   // max |rec - x|
-  uint32_t zor = 0;
+  uint32_t zor = 0;    // OR of the biased codes ZBIAS + z
   auto step = [&](float x) -> uint32_t {
     const float vf = __fmul_rn(__fsub_rn(x, prev32), rtw);
     const float m = __fadd_rn(vf, MAGIC32);
-    frmax = fmaxf(frmax, fabsf(__fsub_rn(vf, __fsub_rn(m, MAGIC32))));
-    const uint32_t qb = (uint32_t)__float_as_int(m) + 0x34C00000u;  // q ^ 0x80000000
-    const double qd = __dsub_rn(__hiloint2double(0x43300000, (int)qb), 4503601774854144.0);
+    const float qf = __fsub_rn(m, MAGIC32);  // q, exact while |vf| < 2^22
+    frmax = fmaxf(frmax, fabsf(__fsub_rn(vf, qf)));
+    // q in binary64 straight from m's bits: (2^52 + bits(m)) - (2^52 + bits(MAGIC32)), one DADD
+    const double qd = __dsub_rn(__hiloint2double(0x43300000, __float_as_int(m)), M52_PLUS_MAGIC32);
     const double t = __dadd_rn(prev64, __dmul_rn(qd, tw));
     prev32 = __double2float_rn(t);
     prev64 = (double)prev32;
     emax = fmaxf(emax, fabsf(__fsub_rn(prev32, x)));
-    // zigzag(q) = (q << 1) ^ (q >> 31) = (qb << 1) ^ ~(qb >> 31): shift, add, one LOP3
-    uint32_t z;
-    asm("{\n\t.reg .b32 s, d;\n\tshr.s32 s, %1, 31;\n\tadd.u32 d, %1, %1;\n\tlop3.b32 %0, d, s, 0, 0xC3;\n\t}"
-        : "=r"(z) : "r"(qb));
+    // zigzag(q) = |2q + 1/2| - 1/2, formed in the f32 pipe as the bits of 2^23 + z (two exact
+    // ops, no integer shift/xor chain); see zbias_valid() for the out-of-range cases
+    const float tz = __fmaf_rn(qf, 2.0f, 0.5f);
+    const uint32_t z = __float_as_uint(__fadd_rn(fabsf(tz), 8388607.5f));
     zor |= z;
     return z;
   };
@@ -245,16 +268,16 @@ __device__ __forceinline__ int fast_block(const float* xs, float* zs, int row, d
     const uint32_t z0 = step(c4.x), z1 = step(c4.y), z2 = step(c4.z), z3 = step(c4.w);
     *reinterpret_cast<uint4*>(zs + xs_index(row, c)) = make_uint4(z0, z1, z2, z3);
   }
-  zor_out = zor;
-  const int w = 32 - __clz(zor);
-  if (w > 21) return FB_SLOW;
+  if (!zbias_valid(zor)) return FB_SLOW;
+  zor_out = zor & ZBIAS_MASK;
+  const int w = 32 - __clz(zor_out);
   const float vmax = __int_as_float((126 + w) << 23) + 0.5f;  // 2^(w-1) + 1/2 (exact; w = 0 gives 1)
   if (!(fmaf(vmax, 0x1p-21f, frmax) < thr)) return FB_SLOW;
   if (emax > ehi) return FB_RAW;             // some error provably > eb
   return emax >= elo ? FB_SLOW : FB_PACKED;  // undecided within 2^-22 of eb
 }
 
-// code j (0..30) of a row written by fast_block / store_codes
+// code j (0..30) of a row written by fast_block / store_codes, biased: ZBIAS + z (mod 2^32)
 __device__ __forceinline__ void load_codes(const float* xs, int row, uint32_t (&z)[31]) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
@@ -268,8 +291,9 @@ __device__ __forceinline__ void load_codes(const float* xs, int row, uint32_t (&
 __device__ __forceinline__ void store_codes(float* xs, int row, float x0, const uint32_t* z) {
 #pragma unroll
   for (int c = 0; c < 8; ++c) {
-    const uint32_t a = c ? z[4 * c - 1] : __float_as_uint(x0);
-    *reinterpret_cast<uint4*>(xs + xs_index(row, c)) = make_uint4(a, z[4 * c], z[4 * c + 1], z[4 * c + 2]);
+    const uint32_t a = c ? z[4 * c - 1] + ZBIAS : __float_as_uint(x0);
+    *reinterpret_cast<uint4*>(xs + xs_index(row, c)) =
+        make_uint4(a, z[4 * c] + ZBIAS, z[4 * c + 1] + ZBIAS, z[4 * c + 2] + ZBIAS);
   }
 }
 
