@@ -86,9 +86,6 @@ inline int dev_sms(int dev) {
 
 // Persistent grid: as many CTAs as fit on the device at once (per device),
 // after opting the kernel into `smem` bytes of dynamic shared memory there.
-#ifndef GZ_FUSED_GATHER
-#define GZ_FUSED_GATHER 0
-#endif
 #ifndef GZ_CARVEOUT_MAX
 #define GZ_CARVEOUT_MAX 0
 #endif
@@ -177,23 +174,6 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   a.gshift = gs;
   a.ngctas = gbase;
   count_launch();
-  if (GZ_FUSED_GATHER && !a.slotted_out) {
-    // one cooperative launch: the encoder grid gathers its own blob after a
-    // grid barrier (all CTAs resident: one per SM)
-    a.fused_gather = 1;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)base);
-    cfg.blockDim = dim3(32 * NW);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k_tile_encode<SRC, NSEG, FAST>, a);
-  }
-  a.fused_gather = 0;
   k_tile_encode<SRC, NSEG, FAST><<<(unsigned)base, 32 * NW, smem, s>>>(a);
   int rc = (int)cudaGetLastError();
   if (rc) return rc;

@@ -60,13 +60,7 @@ struct EncodeArgs {
   int slotted_out;         // 1: the output stays in slotted form (scratch/tile_rel), no gather
   unsigned int* post_flag; // slotted only, may be null: set to 1 once the whole output is written
   unsigned int* wait_flag; // slotted only, may be null: wait until >= 1 before reading inputs, reset to 0
-  int fused_gather;        // 1: the encoder grid (a cooperative launch) gathers the blob itself after a grid barrier
 };
-
-template <int NSEG>
-__device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_t gw, uint64_t nwarps, int lane);
-template <int NSEG>
-__device__ __forceinline__ void gather_retire(const EncodeArgs<NSEG>& a, int* s_last);
 
 
 
@@ -717,29 +711,6 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
-  if (a.fused_gather) {
-    // grid barrier (every CTA is resident: cooperative launch, one CTA per SM):
-    // warps that ran out of tiles wait at the CTA barrier, so they take no
-    // issue slots from the CTA's encoding warps; one thread per CTA spins
-    __shared__ int s_last;
-    __threadfence();
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      atomicAdd(&a.ws->arrive, 1u);
-      unsigned int v;
-      for (;;) {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(&a.ws->arrive) : "memory");
-        if (v >= gridDim.x) break;
-        __nanosleep(64);
-      }
-      __threadfence();
-    }
-    __syncthreads();
-    gather_groups(a, (uint64_t)blockIdx.x * NW + warp, (uint64_t)gridDim.x * NW, lane);
-    gather_retire(a, &s_last);
-    return;
-  }
   if (a.slotted_out) {
     // no gather kernel follows: the last CTA re-zeroes the claim counter and
     // posts the step's completion flag (a peer's, over NVLink) itself, so a
@@ -937,7 +908,7 @@ __device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_
 }
 
 // Retire (every thread of the CTA): the last CTA to get here zeroes the
-// counters (and the grid barrier word) for the next launch.
+// counters for the next launch.
 template <int NSEG>
 __device__ __forceinline__ void gather_retire(const EncodeArgs<NSEG>& a, int* s_last) {
   TileWs* ws = a.ws;
@@ -952,7 +923,6 @@ __device__ __forceinline__ void gather_retire(const EncodeArgs<NSEG>& a, int* s_
     if (tid == 0) {
       ws->done = 0;
       ws->claim = 0;
-      ws->arrive = 0;
     }
   }
 }

@@ -69,8 +69,6 @@ struct TileWs {
   unsigned long long pad0[15];
   unsigned int claim;               // encoder tile claims (own 128-byte line)
   unsigned int pad1[31];
-  unsigned int arrive;              // grid barrier of the fused encoder + gather (own 128-byte line)
-  unsigned int pad2[31];
   unsigned int agg[MAXGRID];
   unsigned int agg2[MAXGRID / 32];
   unsigned int agg3[MAXGRID / 1024];
