@@ -409,6 +409,9 @@ __device__ __forceinline__ void reload_row(const EncodeArgs<NSEG>& a, const Seg&
   }
 }
 
+#ifndef GZ_PACK_SMALL
+#define GZ_PACK_SMALL 1
+#endif
 // Phase A for one warp tile (values in xs): quantise and pack the tile into
 // `dst` starting at byte `pos0`.  In a run (carry mode) the tile continues the
 // previous tile's bytes: `carry` holds that tile's last partial word and the
@@ -494,7 +497,12 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
   const uint32_t next_w = __shfl_down_sync(0xFFFFFFFFu, (uint32_t)wbyte, 1);
   const uint32_t next_x0 = __shfl_down_sync(0xFFFFFFFFu, __float_as_uint(x0), 1);
   uint32_t my_carry = 0;
-  if (active) {
+  const bool small = active && !raw && w <= 4 && cnt == 32;
+  if (GZ_PACK_SMALL && !run_mode && nblk == TB && __all_sync(0xFFFFFFFFu, small)) {
+    uint32_t z[31];
+    load_codes(zs, lane, z);
+    pack_small(dst + (pos0 >> 2), start, w, x0, z, lane + 1 < TB ? (next_w | (next_x0 << 8)) : 0u, pol_keep);
+  } else if (active) {
     Appender ap;
     if (lane == 0 && run_mode) ap.init_carry(dst, pos0, carry);
     else ap.init(dst, pos0 + start, lane == 0);

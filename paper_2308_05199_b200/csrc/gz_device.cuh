@@ -352,6 +352,65 @@ struct Appender {
   }
 };
 
+// Packing fast path for a warp whose 32 blocks are all full, packed (not raw)
+// and of width w <= 4 (most tiles of a smooth field): the lane assembles its
+// whole block -- [w][x0][31 codes LSB-first] (codec.py:244-270) followed by
+// the next block's leading bytes that complete its last word -- as a 192-bit
+// value, shifts it to the block's byte alignment and stores its words, with
+// the same word ownership as Appender (a block whose start is not word
+// aligned leaves its first word to the previous block).  Uniform control
+// flow; ~100 instructions per block instead of ~270 for the streaming
+// Appender.  z: the 31 biased codes (load_codes).
+__device__ __forceinline__ void pack_small(uint32_t* dst, int start, int w, float x0, const uint32_t (&z)[31],
+                                           uint32_t next_lead, uint64_t pol) {
+  const uint32_t P1 = 1u << w, P2 = 1u << (2 * w);
+  const uint32_t K = ZBIAS * (1u + P1) * (1u + P2);  // bias of a quad of biased codes (mod 2^32)
+  uint32_t oct[4];                                     // 8 codes = w bytes each
+#pragma unroll
+  for (int g = 0; g < 4; ++g) {
+    uint32_t pr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int j0 = 8 * g + 2 * i;
+      pr[i] = z[j0] + ((j0 + 1 < 31) ? z[j0 + 1] : ZBIAS) * P1;
+    }
+    const uint32_t qa = pr[0] + pr[1] * P2 - K, qb = pr[2] + pr[3] * P2 - K;
+    oct[g] = qa | (qb << (4 * w));
+  }
+  // codes bitstream C (31 w <= 124 bits) = oct0 | oct1 << 8w | oct2 << 16w | oct3 << 24w
+  const uint64_t A = (uint64_t)oct[0] | ((uint64_t)oct[1] << (8 * w));
+  const uint64_t B = (uint64_t)oct[2] | ((uint64_t)oct[3] << (8 * w));
+  const int sB = 16 * w;  // 0..64
+  const uint64_t Clo = A | (sB < 64 ? (B << sB) : 0ull);
+  const uint64_t Chi = sB == 0 ? 0ull : (sB < 64 ? (B >> (64 - sB)) : B);
+  // block = header (40 bits) | C << 40, then the next block's lead bytes at its end
+  uint64_t S0 = (uint64_t)w | ((uint64_t)__float_as_uint(x0) << 8) | (Clo << 40);
+  uint64_t S1 = (Clo >> 24) | (Chi << 40);
+  uint64_t S2 = Chi >> 24;
+  const int size = 5 + ((31 * w + 7) >> 3);  // codec.py:236, 21 bytes at most
+  const int pb = 8 * size;                    // 40 .. 168
+  const uint64_t NL = next_lead;
+  if (pb < 64) {
+    S0 |= NL << pb;
+    S1 |= NL >> (64 - pb);
+  } else if (pb < 128) {
+    S1 |= NL << (pb - 64);
+    if (pb > 64) S2 |= NL >> (128 - pb);
+  } else {
+    S2 |= NL << (pb - 128);
+  }
+  const uint32_t sw[6] = {(uint32_t)S0, (uint32_t)(S0 >> 32), (uint32_t)S1, (uint32_t)(S1 >> 32), (uint32_t)S2,
+                          (uint32_t)(S2 >> 32)};
+  const int al = start & 3, sh = 8 * al;
+  const int nw = (al + size + 3) >> 2;  // <= 6
+  uint32_t* p = dst + (start >> 2);
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const uint32_t t = __funnelshift_l(k ? sw[k - 1] : 0u, sw[k], sh);
+    if (k < nw && (k > 0 || al == 0)) st_u32_hint(p + k, t, pol);
+  }
+}
+
 // load one 32-value row from the swizzled tile
 __device__ __forceinline__ void load_row(const float* xs, int row, float (&v)[32]) {
 #pragma unroll
