@@ -356,6 +356,12 @@ int decode_one(const uint8_t* blob, const void* sidecar, const float* local, int
 extern "C" {
 
 // profiling only: write the GPU's %globaltimer (ns) into *dst, stream-ordered
+#if GZ_DIAG_STAMPS
+int gz_diag_stamps(void* gst, void* est) {
+  cudaMemcpyFromSymbol(gst, g_gst, sizeof(g_gst));
+  return (int)cudaMemcpyFromSymbol(est, g_est, sizeof(g_est));
+}
+#endif
 int gz_debug_stamp(void* dst, gz_stream_t stream) {
   k_stamp<<<1, 1, 0, (cudaStream_t)stream>>>(reinterpret_cast<unsigned long long*>(dst));
   return (int)cudaGetLastError();

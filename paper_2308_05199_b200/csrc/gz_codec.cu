@@ -14,6 +14,13 @@
 namespace gz {
 
 enum { SRC_PLAIN = 0, SRC_STEP = 1 };
+#ifndef GZ_DIAG_STAMPS
+#define GZ_DIAG_STAMPS 0  // diagnostic builds only (tools/exp/gather_stamps.py)
+#endif
+#if GZ_DIAG_STAMPS
+__device__ unsigned long long g_gst[3 * 8192];   // per gather group: start, base known, copied
+__device__ unsigned long long g_est[256 * 32];   // per encoder warp: end of its tile loop
+#endif
 // report_base value of a kernel whose `local` is NOT the caller's input (e.g. a
 // recursive-doubling step reducing into its output in place): nothing is reported
 constexpr uint64_t NO_REPORT = ~0ull;
@@ -719,6 +726,9 @@ __global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const En
     j1 = j < total ? claim() : total;
   }
   cp_async_wait_all();
+#if GZ_DIAG_STAMPS
+  if (lane == 0 && blockIdx.x < 256) g_est[blockIdx.x * 32 + warp] = gtimer();
+#endif
   if (a.slotted_out) {
     // no gather kernel follows: the last CTA re-zeroes the claim counter and
     // posts the step's completion flag (a peer's, over NVLink) itself, so a
@@ -806,6 +816,9 @@ __device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_
   TileWs* ws = a.ws;
   const uint64_t cend = a.ngctas;
   for (uint64_t c = gw; c < cend; c += nwarps) {
+#if GZ_DIAG_STAMPS
+    if (lane == 0 && c < 8192) g_gst[3 * c] = gtimer();
+#endif
     int k = 0;
     if (NSEG > 1) {
 #pragma unroll 1
@@ -827,7 +840,8 @@ __device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_
     uint4 v[U];
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      v[u] = u < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)u * TILE_SLOT + 16 * lane) : make_uint4(0, 0, 0, 0);
+      v[u] = u < nr ? *reinterpret_cast<const uint4*>(sl0 + (uint64_t)u * TILE_SLOT + 16 * lane)
+                                       : make_uint4(0, 0, 0, 0);
     // bytes of the launch's groups before c minus those before the segment's
     // first group glo: <= 16 + 31 + 31 terms each, one load per lane per level
     auto prefix_terms = [&](uint64_t x) -> unsigned long long {
@@ -838,6 +852,9 @@ __device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_
       return v;
     };
     unsigned long long base = warp_sum_u64(prefix_terms(c) - prefix_terms(glo));  // payload offset of the group
+#if GZ_DIAG_STAMPS
+    if (lane == 0 && c < 8192) g_gst[3 * c + 1] = gtimer() + (base & 0);
+#endif
 
     for (int s0 = 0; s0 < nr; s0 += 32) {  // 32 tiles (one per lane) at a time
       if (s0) sz = s0 + lane < nr ? sizes[s0 + lane] : 0u;
@@ -908,6 +925,9 @@ __device__ __forceinline__ void gather_groups(const EncodeArgs<NSEG>& a, uint64_
       }
       reinterpret_cast<uint32_t*>(S.blob)[lane] = hw;
     }
+#if GZ_DIAG_STAMPS
+    if (lane == 0 && c < 8192) g_gst[3 * c + 2] = gtimer();
+#endif
     if (c == glo + S.gcta_n - 1 && lane == 0) {  // the segment's last group knows the total
       if (S.out_tile_off) S.out_tile_off[G.ntiles] = base;
       *S.out_len = HEADER_BYTES + base;
