@@ -226,8 +226,8 @@ def e2e_codec(gz, xp, ws_list, streams, total_steps: int, ref_blob: bytes):
     compress(pinned f32 host tensor) -> pinned host blob (H2D of the input, the
     kernels, D2H of the blob), then decompress(host blob) -> pinned host f32
     (H2D of the blob, device indexing of the reference bytes, decode, D2H).
-    Two steps are in flight on two streams (separate workspaces), so one step's
-    H2D overlaps the other's D2H on the full-duplex link."""
+    Several steps are in flight on as many streams (separate workspaces), so one
+    step's H2D overlaps another's D2H on the full-duplex link."""
     import torch
 
     lanes = len(streams)
@@ -397,13 +397,17 @@ def bench_codec(args):
         big = {"error": str(e)[:200]}
     torch.cuda.empty_cache()
 
-    # e2e through the public API with pinned host buffers, two steps in flight
+    # e2e through the public API with pinned host buffers, several steps in flight
     xp = torch.from_numpy(xh).pin_memory()
-    lanes = 3  # steps in flight (tools/exp/e2e_lanes.py: 49 / 64 / 77 GB/s for 1 / 2 / 3, 4 collapses)
+    # steps in flight: tools/exp/e2e_var.py, six runs each after warm-up: 2 lanes 63-66 GB/s,
+    # 3 lanes 72-81, 4 lanes 76-83 (the first run after a short warm-up collapses while the
+    # pinned host pools fill, hence the longer warm-up)
+    lanes = 4
     e2e_ws = [gz.Workspace(dev) for _ in range(lanes)]
     e2e_streams = [torch.cuda.Stream(dev) for _ in range(lanes)]
-    e2e_steps = max(8, min(args.steps, 20))
-    e2e_codec(gz, xp, e2e_ws, e2e_streams, 2 * lanes, ref_blob)  # warm-up (pinned pools, index workspaces)
+    e2e_steps = max(8, min(2 * args.steps, 40))
+    for _ in range(2):  # warm-up (pinned host pools, index workspaces)
+        e2e_codec(gz, xp, e2e_ws, e2e_streams, 3 * lanes, ref_blob)
     wall, y_last = e2e_codec(gz, xp, e2e_ws, e2e_streams, e2e_steps, ref_blob)
     assert y_last.numpy().tobytes() == ref_y.tobytes(), "e2e decode differs from the oracle"
     parity["e2e"] = "bit-exact vs oracle (host blob and host values)"
