@@ -221,6 +221,17 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 
 
+def _traffic(key: str):
+    """DRAM bytes per launch of the line's dominant kernel, from the committed ncu capture
+    (profiles/traffic.json, with the command and capture it came from); None if absent."""
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(tp) as f:
+            return json.load(f).get(key)
+    except Exception:
+        return None
+
+
 def e2e_codec(gz, xp, ws_list, streams, total_steps: int, ref_blob: bytes):
     """End to end through the public API from pinned host memory: each step =
     compress(pinned f32 host tensor) -> pinned host blob (H2D of the input, the
@@ -418,14 +429,7 @@ def bench_codec(args):
     cpu_gbs2, cpu_t2 = cpu_codec_round_trip(xh, EB, thr_all)
     cpu_gbs = max(cpu_gbs, cpu_gbs2)
 
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get("compress_cfg1")
-        except Exception:
-            traffic = None
+    traffic = _traffic("compress_cfg1")
     line = _line(
         1, args.steps, warm, round(value, 2), round((t_c + t_d) * 1e3, 5), shared_config(1),
         detail={"value_is": "codec round trip: (bytes of compress + bytes of decompress) / (compress + decompress "
@@ -696,7 +700,7 @@ def bench_allreduce(args):
                     "rd_allreduce_gbs": round(rd_gbs, 2)},
             roofline={"bound": "hbm", "kernel": "fused RS step (k_tile_encode<STEP>, slotted output)",
                       "achieved": round(step_gbs, 1), "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                      "frac": round(step_gbs / peak, 4), "traffic": None,
+                      "frac": round(step_gbs / peak, 4), "traffic": _traffic(f"fused_step_peer_{m}"),
                       "algorithmic_bytes_per_launch": int(step_bytes), "avg_step_us": round(t_step * 1e6, 2),
                       "bytes_per_unit": "4 B local + received and produced compressed bytes per value"},
             cpu_baseline=cpu_base,
