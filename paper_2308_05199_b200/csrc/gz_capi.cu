@@ -86,20 +86,12 @@ inline int dev_sms(int dev) {
 
 // Persistent grid: as many CTAs as fit on the device at once (per device),
 // after opting the kernel into `smem` bytes of dynamic shared memory there.
-#ifndef GZ_CARVEOUT_MAX
-#define GZ_CARVEOUT_MAX 0
-#endif
 template <typename K>
 int grid_cap(K kernel, int threads, size_t smem, int (&cache)[MAXDEV]) {
   const int dev = cur_dev();
   if (cache[dev] == 0) {
     int occ = 0;
     if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-#if GZ_CARVEOUT_MAX
-    // every kernel of the library asks for the same L1/shared split, so consecutive
-    // launches (encoder -> gather -> decoder) never wait for an SM to be reconfigured
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
-#endif
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem);
     cache[dev] = (occ > 0 ? occ : 1) * dev_sms(dev) + 1;
   }
