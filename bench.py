@@ -232,6 +232,22 @@ def _traffic(key: str):
         return None
 
 
+def _issue_roofline(t_compress: float):
+    """The compressor's instruction-issue floor: warp-instructions per call
+    from the committed ncu capture / (SMs x 4 schedulers x SM clock), against the measured
+    compress time."""
+    ins = _traffic("compress_cfg1_warp_instructions")
+    if not ins:
+        return None
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    clk_hz = 1.965e9  # B200 boost clock (the bench's clock sampler shows 1965 MHz under load)
+    floor = ins / (sms * 4 * clk_hz)
+    return {"warp_instructions_per_call": ins, "issue_floor_us": round(floor * 1e6, 2),
+            "frac": round(floor / t_compress, 4), "source": "profiles/traffic.json (ncu instruction counts)"}
+
+
 def e2e_codec(gz, xp, ws_list, streams, total_steps: int, ref_blob: bytes):
     """End to end through the public API from pinned host memory: each step =
     compress(pinned f32 host tensor) -> pinned host blob (H2D of the input, the
@@ -436,7 +452,8 @@ def bench_codec(args):
                             "device time)", "compressed_bytes": Lb, "compression_ratio": round(4 * n / Lb, 4),
                 "compress_us": round(t_c * 1e6, 2), "decompress_us": round(t_d * 1e6, 2),
                 "compressor_hbm_gbs": round(achieved_c, 1), "decompressor_hbm_gbs": round(bytes_d / t_d / 1e9, 1),
-                "codec_2p27": big},
+                "codec_2p27": big,
+                "issue_roofline": _issue_roofline(t_c)},
         roofline={"bound": "hbm", "kernel": "compressor (k_tile_encode + k_gather)", "achieved": round(achieved_c, 1),
                   "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved_c / peak, 4),
                   "traffic": traffic, "algorithmic_bytes_per_launch": bytes_c,
