@@ -313,9 +313,28 @@ PFN_batchMemOp p_batch() {
 
 
 namespace {
+// Tensor map of the decoder's output for TMA tensor stores (k_tile_decode): y viewed as
+// [n/32 rows][32 floats], box 32 x 32, 128-byte swizzle.  Returns 0 (plain stores)
+// when y is not 16-byte aligned, has no full tile, or the driver refuses the map.
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int encode_ymap(CUtensorMap* map, float* y, uint64_t n) {
+  static PFN_encodeTiled f = driver_fn<PFN_encodeTiled>("cuTensorMapEncodeTiled");
+  const uint64_t rows = n / BLOCK;
+  if (!f || !y || (reinterpret_cast<uintptr_t>(y) & 15) || rows < (uint64_t)TB || rows > 0x7FFFFFFFull) return 0;
+  const cuuint64_t dims[2] = {BLOCK, rows};
+  const cuuint64_t strides[1] = {BLOCK * sizeof(float)};
+  const cuuint32_t box[2] = {BLOCK, TB};
+  const cuuint32_t estr[2] = {1, 1};
+  return f(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, y, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int NSEG>
 int launch_decode(DecodeMultiArgs<NSEG>& a, cudaStream_t s, int reserve_sms = 0) {
-  const size_t smem = (size_t)WARPS * dec_warp_smem(NSEG);  // per warp: value tile + stagings
+  const size_t smem = (size_t)dec_cta_smem(NSEG);  // per warp: value tile + stagings (+ alignment slack)
   static int caps[MAXDEV];
   const int cap = grid_cap(k_tile_decode<NSEG>, CTA_THREADS, smem, caps);
   const int per_sm = std::max(1, cap / dev_sms(cur_dev()));
@@ -340,6 +359,7 @@ int decode_one(const uint8_t* blob, const void* sidecar, const float* local, int
   a.local = local;
   a.op = op;
   a.st = reinterpret_cast<Status*>(d_status);
+  if (!local) a.ytma = encode_ymap(&a.ymap, y, n);
   return launch_decode<1>(a, (cudaStream_t)stream);
 }
 

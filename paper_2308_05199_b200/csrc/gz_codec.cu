@@ -987,23 +987,46 @@ struct DecodeMultiArgs {
   int op;
   Status* st;
   uint64_t report_base;    // offset of local[0] in the caller's buffer (first_nonfinite reports)
+  // NSEG == 1, no `local`: full tiles leave shared memory through ONE TMA tensor store
+  // (cp.async.bulk.tensor) instead of 8 loads + 8 stores per lane.  ymap views y as
+  // [n/32 rows][32 floats] with a 32 x 32 box and the 128-byte swizzle, which is
+  // exactly the xs layout (16-byte chunk index XOR row & 7 inside 128-byte rows).
+  int ytma;
+  CUtensorMap ymap;
 };
+
+// TMA tensor store of one 32 x 32 box (the swizzled tile at shared address sx) to
+// rows [row, row + 32) of the map; bulk async group of the issuing thread.
+__device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, unsigned sx, int row) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+               ::"l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(row), "r"(sx) : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Stages per warp: 2 (one tile ahead), also for peer memory
 // (three stages for the multi-owner allgather measured 3 % slower at N = 4 once
 // the slotted sizes stay in flight, fewer resident warps)
 __host__ __device__ constexpr int dec_stages(int nseg) { return 2; }
 __host__ __device__ constexpr int dec_warp_smem(int nseg) { return TILE_VALUES * 4 + dec_stages(nseg) * STAGE_BYTES; }
+// dynamic shared memory of a decoder CTA: the warps' value tiles first (1024-byte
+// aligned, as the 128-byte TMA swizzle requires), then their staging buffers
+constexpr int DEC_SMEM_ALIGN = 1024;
+__host__ __device__ constexpr int dec_cta_smem(int nseg) { return DEC_SMEM_ALIGN + WARPS * dec_warp_smem(nseg); }
 
 template <int NSEG>
-__global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiArgs<NSEG> a) {
+__global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const __grid_constant__ DecodeMultiArgs<NSEG> a) {
   constexpr int ST = dec_stages(NSEG), D = ST - 1;  // D tiles staged ahead
-  extern __shared__ __align__(128) unsigned char smem[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ double s_step[256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  unsigned char* my = smem + warp * dec_warp_smem(NSEG);
-  float* xs = reinterpret_cast<float*>(my);
-  uint32_t* stg = reinterpret_cast<uint32_t*>(my + TILE_VALUES * 4);
+  const unsigned sraw = (unsigned)__cvta_generic_to_shared(smem_raw);
+  unsigned char* smem = smem_raw + (((sraw + DEC_SMEM_ALIGN - 1) & ~(unsigned)(DEC_SMEM_ALIGN - 1)) - sraw);
+  float* xs = reinterpret_cast<float*>(smem + warp * TILE_VALUES * 4);
+  uint32_t* stg = reinterpret_cast<uint32_t*>(smem + WARPS * TILE_VALUES * 4 + warp * ST * STAGE_BYTES);
+  const unsigned xs_s = (unsigned)__cvta_generic_to_shared(xs);
+  const bool tma = NSEG == 1 && a.ytma && !a.local;
   init_step_table(s_step, a.tw);
   __syncthreads();
   const uint64_t total = a.total_tiles;
@@ -1084,10 +1107,22 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     const int nval = (int)(n - v0 < (uint64_t)TILE_VALUES ? n - v0 : (uint64_t)TILE_VALUES);
     const int wl = lane < nblk ? wq[0] : 0;
     const int start = block_start(stage_t, bq[0], (int)(md[0].te - md[0].ts), wl, nblk, b0, nb, last_cnt, a.st, lane);
+    if (tma) {  // the previous tile's TMA store must have read xs before it is overwritten
+      if (lane == 0) tma_wait_read();
+      __syncwarp();
+    }
     decode_row<0>(stage_t, bq[0], start, wl, b0, nb, last_cnt, a.tw, xs, 0, s_step, lane);
     __syncwarp();
-    if (NSEG == 1 && a.local) drain_values_op(xs, a.local, a.op, S.y, v0, nval, lane, a.st, a.report_base);
-    else drain_values(xs, S.y, v0, nval, lane);
+    if (tma && nval == TILE_VALUES) {
+      // generic-proxy writes of xs -> visible to the async (TMA) proxy, then one store
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tma_store_tile(&a.ymap, xs_s, (int)b0);
+    } else if (NSEG == 1 && a.local) {
+      drain_values_op(xs, a.local, a.op, S.y, v0, nval, lane, a.st, a.report_base);
+    } else {
+      drain_values(xs, S.y, v0, nval, lane);
+    }
     __syncwarp();
 #pragma unroll
     for (int d = 0; d + 1 < D; ++d) {
@@ -1101,6 +1136,7 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const DecodeMultiAr
     mnext = mnn;
     bi = (bi + 1) % ST;
   }
+  if (tma && lane == 0) tma_wait_all();
 }
 
 }  // namespace gz
