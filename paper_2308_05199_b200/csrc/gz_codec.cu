@@ -1005,6 +1005,9 @@ __device__ __forceinline__ void tma_store_tile(const CUtensorMap* map, unsigned 
 __device__ __forceinline__ void tma_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+#ifndef GZ_DEC_BULK
+#define GZ_DEC_BULK 1
+#endif
 // Stages per warp: 2 (one tile ahead), also for peer memory
 // (three stages for the multi-owner allgather measured 3 % slower at N = 4 once
 // the slotted sizes stay in flight, fewer resident warps)
@@ -1027,6 +1030,21 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const __grid_consta
   uint32_t* stg = reinterpret_cast<uint32_t*>(smem + WARPS * TILE_VALUES * 4 + warp * ST * STAGE_BYTES);
   const unsigned xs_s = (unsigned)__cvta_generic_to_shared(xs);
   const bool tma = NSEG == 1 && a.ytma && !a.local;
+  // every decode but the codec's own (which stores through TMA and stages with cp.async,
+  // measured slightly faster at cfg1) stages the compressed tiles with TMA bulk copies --
+  // typically out of a peer's memory (allgather, scatter): one large NVLink read per tile
+  // instead of 16-byte pieces per lane; one mbarrier per staging buffer
+  const bool bulk = GZ_DEC_BULK && !tma;
+  __shared__ __align__(8) unsigned long long s_mbar[WARPS][2];
+  const unsigned mbar_s = (unsigned)__cvta_generic_to_shared(&s_mbar[warp][0]);
+  const unsigned stg_s = (unsigned)__cvta_generic_to_shared(stg);
+  unsigned ph = 0;  // bit b: parity of buffer b's next completion
+  if (bulk && lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_s) : "memory");
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar_s + 8) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   init_step_table(s_step, a.tw);
   __syncthreads();
   const uint64_t total = a.total_tiles;
@@ -1068,7 +1086,30 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const __grid_consta
       // block_start() then reports the mismatch (checked here, where the offsets
       // are consumed, so their loads stay in flight behind the previous tile)
       if (m.te < m.ts || m.te - m.ts > (uint64_t)TB * MAX_BLOCK_BYTES) m.te = m.ts;
-      base = stage_bytes<true>(stg + bi * STAGE_WORDS, S.sizes ? S.blob : S.blob + HEADER_BYTES, m.ts, m.te, lane);
+      const uint8_t* src = S.sizes ? S.blob : S.blob + HEADER_BYTES;
+      if (bulk) {
+        // one TMA bulk copy of the tile's 16-byte-aligned byte range (typically a peer's
+        // memory: one large NVLink read instead of 16-byte pieces per lane), completing
+        // on this buffer's mbarrier; the proxy fence orders the buffer's previous generic
+        // reads before the async-proxy write
+        const uintptr_t a0 = (reinterpret_cast<uintptr_t>(src) + m.ts) & ~(uintptr_t)15;
+        const uintptr_t a1 = (reinterpret_cast<uintptr_t>(src) + m.te + 15) & ~(uintptr_t)15;
+        const unsigned nbytes = (unsigned)(a1 - a0);
+        if (lane == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar_s + 8 * bi), "r"(nbytes)
+                       : "memory");
+          if (nbytes)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    stg_s + bi * STAGE_BYTES),
+                "l"(a0), "r"(nbytes), "r"(mbar_s + 8 * bi)
+                : "memory");
+        }
+        base = (int)((reinterpret_cast<uintptr_t>(src) + m.ts) & 15);
+      } else {
+        base = stage_bytes<true>(stg + bi * STAGE_WORDS, src, m.ts, m.te, lane);
+      }
       w = S.widths[(t - S.tile_base) * TB + lane];
     }
   };
@@ -1092,8 +1133,18 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const __grid_consta
     cp_async_commit();
     const Meta mnn = offsets(tn + stride);
     // wait until tile t's group is complete (D newer groups may stay pending)
-    if (D == 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-    else cp_async_wait_1();
+    if (bulk) {
+      unsigned done = 0;
+      const unsigned par = (ph >> bi) & 1u;
+      while (!done)
+        asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(mbar_s + 8 * bi), "r"(par) : "memory");
+      ph ^= 1u << bi;
+    } else if (D == 2) {
+      asm volatile("cp.async.wait_group 2;" ::: "memory");
+    } else {
+      cp_async_wait_1();
+    }
     __syncwarp();
     const uint32_t* stage_t = stg + bi * STAGE_WORDS;
     const DecSeg& S = a.seg[seg_of(t)];
