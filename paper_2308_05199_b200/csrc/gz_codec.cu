@@ -167,11 +167,31 @@ __device__ __forceinline__ void drain_values_op(const float* xs, const float* __
                                                 float* __restrict__ dst, uint64_t v0, int nval, int lane,
                                                 Status* st, uint64_t report_base) {
   bool bad = false;
+  if (nval == TILE_VALUES && (((reinterpret_cast<uintptr_t>(local + v0) | reinterpret_cast<uintptr_t>(dst + v0)) & 15) == 0)) {
+    // full, aligned tile: float4 loads / stores (like drain_values)
+    const float4* l4 = reinterpret_cast<const float4*>(local + v0);
+    float4* d4 = reinterpret_cast<float4*>(dst + v0);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int i = lane + 32 * j;
+      const float4 d = *reinterpret_cast<const float4*>(xs + xs_index(i >> 3, i & 7));
+      const float4 l = __ldcs(l4 + i);
+      bad |= !(isfinite(l.x) && isfinite(l.y) && isfinite(l.z) && isfinite(l.w));
+      float4 o;
+      if (op == 0) {
+        o.x = __fadd_rn(l.x, d.x); o.y = __fadd_rn(l.y, d.y); o.z = __fadd_rn(l.z, d.z); o.w = __fadd_rn(l.w, d.w);
+      } else {
+        o.x = np_maximum_f(l.x, d.x); o.y = np_maximum_f(l.y, d.y); o.z = np_maximum_f(l.z, d.z); o.w = np_maximum_f(l.w, d.w);
+      }
+      __stcs(d4 + i, o);
+    }
+  } else {
   for (int i = lane; i < nval; i += 32) {
     const int row = i >> 5, col = i & 31;
     const float d = xs[xs_index(row, col >> 2) + (col & 3)], l = __ldcs(local + v0 + i);
     bad |= !isfinite(l);
     __stcs(dst + v0 + i, op == 0 ? __fadd_rn(l, d) : np_maximum_f(l, d));
+  }
   }
   if (__any_sync(0xFFFFFFFFu, bad) && report_base != NO_REPORT) {
     for (int i = lane; i < nval; i += 32)
