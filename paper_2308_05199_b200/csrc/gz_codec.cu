@@ -1131,6 +1131,10 @@ __global__ void __launch_bounds__(CTA_THREADS) k_tile_decode(const __grid_consta
         base = stage_bytes<true>(stg + bi * STAGE_WORDS, src, m.ts, m.te, lane);
       }
       w = S.widths[(t - S.tile_base) * TB + lane];
+      if (NSEG == 1 && a.local) {  // warm L2 with this tile's local values (read by the drain)
+        const uint64_t v1 = (t - S.tile_base) * TILE_VALUES + (uint64_t)lane * 32;
+        if (v1 < S.n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a.local + v1));
+      }
     }
   };
   const uint64_t stride = (uint64_t)gridDim.x * WARPS;
