@@ -606,9 +606,9 @@ __device__ __forceinline__ int encode_tile(const EncodeArgs<NSEG>& a, const Seg&
 // tile is packed into its own 128-byte aligned scratch slot (L2 evict_last)
 // and its size recorded; a warp with no tile left simply exits.  The
 // position-independent parts of the sidecar (sub-offsets) are final here.
-template <int SRC, int NSEG, bool FAST>
-__global__ void __launch_bounds__(32 * enc_warps(SRC), 1) k_tile_encode(const EncodeArgs<NSEG> a) {
-  constexpr int NW = enc_warps(SRC);
+template <int SRC, int NSEG, bool FAST, int NWT = 0>
+__global__ void __launch_bounds__(32 * (NWT ? NWT : enc_warps(SRC)), 1) k_tile_encode(const EncodeArgs<NSEG> a) {
+  constexpr int NW = NWT ? NWT : enc_warps(SRC);  // NWT: small-message instance (one tile per CTA)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ double s_step[SRC == SRC_STEP ? 256 : 1];
   __shared__ unsigned int s_next;
