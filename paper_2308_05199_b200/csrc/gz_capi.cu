@@ -180,10 +180,14 @@ int launch_encode_t(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   return (int)cudaGetLastError();
 }
 
-// a message of at most one tile per SM runs one tile per CTA: 4-warp CTAs (32 KB of
-// shared memory instead of 192 KB) launch and retire faster (1 MiB/rank allreduce at
-// N = 2: compress 11.6 -> 8.9 us, fused step 21.7 -> 20.1 us)
-constexpr uint64_t SMALL_MSG_TILES = 148;
+// a small message (up to ~4 tiles per SM) runs one tile per CTA in 4-warp CTAs (32 KB of
+// shared memory instead of 192 KB), which launch and retire faster (1 MiB/rank allreduce
+// at N = 2: compress 11.6 -> 8.9 us, fused step 21.7 -> 20.1 us; 2-4 MiB/rank 76-79 ->
+// 72-74 us per call with the threshold at 600 tiles instead of 148)
+#ifndef GZ_SMALL_MSG_TILES
+#define GZ_SMALL_MSG_TILES 600
+#endif
+constexpr uint64_t SMALL_MSG_TILES = GZ_SMALL_MSG_TILES;
 template <int SRC, int NSEG>
 int launch_encode(EncodeArgs<NSEG>& a, uint64_t total_tiles, cudaStream_t s) {
   if constexpr (NSEG == 1) {
